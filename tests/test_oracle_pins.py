@@ -1,0 +1,356 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (-m "not gpu").
+
+Each test names the passage (PAPER.md line, "P:n") or the mathematical fact it relies on.
+None of them re-types the oracle's own formula: they use printed values (tests/golden/),
+closed forms, brute force on tiny inputs, invariants, or a second, independent algorithm.
+"""
+import itertools
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import seeded_inputs as si
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _read_golden(name):
+    rows = []
+    with open(os.path.join(GOLD, name)) as fh:
+        for line in fh:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line)
+    return rows
+
+
+# ------------------------------------------------------------------ primitives (hand values)
+def test_f_g_hand_values():
+    """eq:f P:295-302 / eq:g P:304-315; hand-evaluated examples."""
+    assert oracle.f_f32(2.0, -3.0) == -2.0
+    assert oracle.f_f32(0.0, 7.0) == 0.0
+    assert [oracle.f_f32(5, -3), oracle.f_f32(2, -7)] == [-3.0, -2.0]
+    assert oracle.g_f32(2.0, 3.0, 0) == 5.0
+    assert oracle.g_f32(2.0, 3.0, 1) == 1.0
+    # G_0R = g with beta_l = 0: g_0r([7,-2,3,9]) -> [10, 7]
+    assert [oracle.g_f32(7, 3, 0), oracle.g_f32(-2, 9, 0)] == [10.0, 7.0]
+    # int8: saturating adders, range [-127,127] (Listing 4's max(-127))
+    assert oracle.g_i8(100, 100, 0) == 127
+    assert oracle.g_i8(100, -100, 1) == -127
+    assert oracle.g_i8(-127, -127, 0) == -127
+    assert oracle.g_i8(127, -127, 1) == -127
+    assert oracle.f_i8(-127, 5) == -5
+    assert oracle.f_i8(-127, -127) == 127
+
+
+def test_rep_spc_hand_values():
+    """Repetition P:431-440 (sum >= 0 -> 0), SPC P:442-459 (flip argmin |alpha|)."""
+    assert list(oracle.rep_node(np.array([-1, 2, -3, 1], np.float32))) == [1, 1, 1, 1]
+    assert list(oracle.rep_node(np.array([0, 0], np.float32))) == [0, 0]
+    assert list(oracle.rep_node(np.array([5, -1], np.int8))) == [0, 0]
+    assert list(oracle.spc_node(np.array([2, -1, 3, 4], np.float32))) == [0, 0, 0, 0]
+    assert list(oracle.spc_node(np.array([1, 1], np.float32))) == [0, 0]
+    # N_v = 4 tie: all |alpha| equal, lowest index flipped (reading C10)
+    assert list(oracle.spc_node(np.array([-1, -1, -1, 1], np.float32))) == [0, 1, 1, 0]
+    assert list(oracle.spc_node(np.array([-1, -1, -1, 1], np.int8))) == [0, 1, 1, 0]
+
+
+# ------------------------------------------------------------------ encoder
+def test_g4_matches_paper():
+    """G_4 printed at P:142-151: row i of G is the encoding of the unit vector e_i."""
+    rows = _read_golden("g4_paper.txt")
+    for i in range(4):
+        e = np.zeros(4, np.uint8); e[i] = 1
+        assert "".join(map(str, oracle.encode_matrix(e))) == rows[i]
+        assert "".join(map(str, oracle.encode(e[None])[0])) == rows[i]
+
+
+@pytest.mark.parametrize("N", [2, 4, 8, 16, 64, 256])
+def test_encode_block_form_equals_kronecker_definition(N):
+    """Block recursion G_N = [G 0; G G] equals the Kronecker definition."""
+    rng = np.random.default_rng(N)
+    for _ in range(8):
+        u = rng.integers(0, 2, N, dtype=np.uint8)
+        assert np.array_equal(oracle.encode(u[None])[0], oracle.encode_matrix(u))
+
+
+@pytest.mark.parametrize("N", [8, 128, 2048])
+def test_encode_is_involution(N):
+    """F_2^{(x)n} squared is the identity over GF(2) (F_2^2 = I)."""
+    rng = np.random.default_rng(1 + N)
+    u = rng.integers(0, 2, (4, N), dtype=np.uint8)
+    assert np.array_equal(oracle.encode(oracle.encode(u)), u)
+
+
+@pytest.mark.parametrize("N,K,ebn0", [(8, 5, 2.0), (64, 32, 2.0), (1024, 512, 2.5), (2048, 1723, 4.0)])
+def test_systematic_encoder(N, K, ebn0):
+    """Systematic codeword: x[A] = d, and u = x G has u[F] = 0 (x is a codeword)."""
+    frozen = oracle.construct_ga(N, K, ebn0)
+    bits, _ = si.draw(7, 0, 6, K, N)
+    x = oracle.encode_systematic(frozen, bits)
+    assert np.array_equal(x[:, frozen == 0], bits)
+    u = oracle.encode(x)
+    assert not u[:, frozen == 1].any()
+
+
+def test_systematic_encoder_arbitrary_mask():
+    """The oracle's systematic encoder is exact for any frozen set (not only
+    superset-closed ones)."""
+    for seed in range(6):
+        frozen = si.random_mask(seed, 32, 13)
+        bits, _ = si.draw(seed, 0, 3, 13, 32)
+        x = oracle.encode_systematic(frozen, bits)
+        assert np.array_equal(x[:, frozen == 0], bits)
+        assert not oracle.encode(x)[:, frozen == 1].any()
+
+
+# ------------------------------------------------------------------ Listing 1 and the worked frame
+def test_listing1_op_sequence():
+    """O2's op sequence on the (8,5) frozen={0,1,4} code is Listing 1."""
+    rows = _read_golden("listing1_8_5.txt")
+    frozen = np.array([int(c) for c in rows[0]], np.uint8)
+    assert oracle.fastssc_trace(frozen) == rows[1:]
+
+
+def test_worked_8_5_frame():
+    """Hand-worked f32 frame (golden/worked_8_5_f32.txt): Fast-SSC and plain SC give the
+    traced codeword; SC's leaf decisions u_hat are x_hat G."""
+    g = {r.split()[0]: r.split()[1:] for r in _read_golden("worked_8_5_f32.txt")}
+    frozen = np.array(g["frozen"], np.uint8)
+    a = np.array(g["alpha_c"], np.float32)[None]
+    xhat = np.array(g["xhat"], np.uint8)
+    assert np.array_equal(oracle.fastssc_decode(frozen, a)[0], xhat)
+    xs, us, zd = oracle.sc_decode(frozen, a, with_stats=True)
+    assert np.array_equal(xs[0], xhat)
+    assert np.array_equal(us[0], np.array(g["uhat"], np.uint8))
+    assert np.array_equal(oracle.info_bits(frozen, xs[0]), np.array(g["info"], np.uint8))
+    # intermediate values of the hand trace
+    f8 = [oracle.f_f32(a[0, i], a[0, i + 4]) for i in range(4)]
+    assert f8 == [float(v) for v in g["f8"]]
+    g0r = [oracle.g_f32(f8[i], f8[i + 2], 0) for i in range(2)]
+    assert g0r == [float(v) for v in g["g0r4"]]
+    g8 = [oracle.g_f32(a[0, i], a[0, i + 4], 1) for i in range(4)]
+    assert g8 == [float(v) for v in g["g8"]]
+
+
+# ------------------------------------------------------------------ node decoders are ML (brute force)
+def _ml_over(words, alpha):
+    """Brute-force correlation metric of every codeword (rows of `words`)."""
+    metric = (1.0 - 2.0 * words.astype(np.float64)) @ alpha.astype(np.float64)
+    return metric.max(), metric
+
+
+@pytest.mark.parametrize("n", [2, 4, 8, 16])
+def test_rep_and_spc_nodes_are_ml(n):
+    """The Repetition and SPC rules return an ML codeword of their node code
+    (brute force over all codewords; exact for continuous inputs, and an ML member of the
+    optimal set for int8 ties)."""
+    rng = np.random.default_rng(100 + n)
+    rep_words = np.stack([np.zeros(n, np.uint8), np.ones(n, np.uint8)])
+    allw = np.array(list(itertools.product([0, 1], repeat=n)), np.uint8)
+    spc_words = allw[allw.sum(axis=1) % 2 == 0]
+    for trial in range(300):
+        a = rng.standard_normal(n).astype(np.float32)
+        for words, fn in ((rep_words, oracle.rep_node), (spc_words, oracle.spc_node)):
+            out = fn(a)
+            best, metric = _ml_over(words, a)
+            winners = np.flatnonzero(metric == best)
+            assert len(winners) == 1 and np.array_equal(out, words[winners[0]])
+        q = rng.integers(-6, 7, n).astype(np.int8)
+        for words, fn in ((rep_words, oracle.rep_node), (spc_words, oracle.spc_node)):
+            out = fn(q)
+            best, metric = _ml_over(words, q)
+            assert (words == out).all(axis=1).any()
+            assert float(np.sum((1.0 - 2.0 * out) * q.astype(np.float64))) == best
+
+
+def _all_masks(N):
+    for bits in itertools.product([0, 1], repeat=N):
+        if 0 < N - sum(bits) <= N:
+            yield np.array(bits, np.uint8)
+
+
+def test_fastssc_is_ml_when_root_is_a_special_node():
+    """For N <= 8 codes whose root is Rate-1 / Rep / SPC, Fast-SSC = brute-force ML (O3);
+    for every other mask O3's metric bounds Fast-SSC's and the output is a codeword."""
+    rng = np.random.default_rng(5)
+    for N in (2, 4, 8):
+        for frozen in _all_masks(N):
+            a = rng.standard_normal((20, N)).astype(np.float32)
+            ml = oracle.ml_decode(frozen, a)
+            fs = oracle.fastssc_decode(frozen, a)
+            kind = oracle.classify(frozen)
+            mm = np.sum((1.0 - 2.0 * ml) * a, axis=1)
+            mf = np.sum((1.0 - 2.0 * fs) * a, axis=1)
+            assert np.all(mf <= mm + 1e-5)
+            assert not oracle.encode(fs)[:, frozen == 1].any()
+            if kind in ("Rate1", "Rep", "SPC"):
+                assert np.array_equal(ml, fs)
+
+
+# ------------------------------------------------------------------ SC == Fast-SSC (two algorithms)
+def _frames(N, K, ebn0, n, seed, i8=False):
+    frozen = oracle.construct_ga(N, K, ebn0)
+    bits, noise = si.draw(seed, 0, n, K, N)
+    x = oracle.encode_systematic(frozen, bits)
+    llr = si.bpsk_awgn_llr(x, noise, ebn0, K)
+    if i8:
+        llr = si.quantize_i8(llr)
+    return frozen, bits, x, llr
+
+
+@pytest.mark.parametrize("N,K,ebn0", [(64, 32, 1.5), (256, 128, 2.0), (1024, 512, 2.5), (2048, 1723, 4.0)])
+def test_sc_equals_fastssc_f32(N, K, ebn0):
+    """f32: plain SC (O1) and Fast-SSC (O2) take identical decisions on every frame with no
+    exactly-zero hard decision (SURVEY 8(c) pin 5; Rate-1 proof in Appendix A; Rep and
+    SPC agree with SC under reading C13 / because SC on an SPC node is the Wagner rule)."""
+    frozen, bits, x, llr = _frames(N, K, ebn0, 400, 11)
+    xs, _, zd = oracle.sc_decode(frozen, llr, with_stats=True)
+    xf = oracle.fastssc_decode(frozen, llr)
+    clean = zd == 0
+    assert clean.mean() > 0.95
+    assert np.array_equal(xs[clean], xf[clean])
+
+
+@pytest.mark.parametrize("N,K,ebn0", [(256, 128, 2.0), (1024, 512, 2.5), (2048, 1723, 4.0)])
+def test_sc_equals_fastssc_i8(N, K, ebn0):
+    """int8: O1 == O2 on frames where SC took no decision on an exact zero (pin 6)."""
+    frozen, bits, x, llr = _frames(N, K, ebn0, 400, 12, i8=True)
+    xs, _, zd = oracle.sc_decode(frozen, llr, with_stats=True)
+    xf = oracle.fastssc_decode(frozen, llr)
+    clean = zd == 0
+    assert clean.mean() > 0.5
+    assert np.array_equal(xs[clean], xf[clean])
+
+
+def test_sc_equals_fastssc_random_masks():
+    """Same agreement on arbitrary (non-constructed) frozen sets, f32."""
+    for seed in range(10):
+        N = [16, 32, 64, 128][seed % 4]
+        K = 1 + (seed * 37) % (N - 1)
+        frozen = si.random_mask(seed, N, K)
+        llr = si.random_llr_f32(seed, (50, N))
+        xs, _, zd = oracle.sc_decode(frozen, llr, with_stats=True)
+        xf = oracle.fastssc_decode(frozen, llr)
+        clean = zd == 0
+        assert np.array_equal(xs[clean], xf[clean])
+
+
+# ------------------------------------------------------------------ invariants
+@pytest.mark.parametrize("i8", [False, True])
+def test_outputs_are_codewords_and_noiseless_roundtrip(i8):
+    """Every decoder output is a codeword ((xhat G)[F] = 0), and a noiseless frame
+    decodes to the transmitted codeword (x[A] = d)."""
+    N, K = 1024, 512
+    frozen, bits, x, llr = _frames(N, K, 2.5, 200, 13, i8=i8)
+    for dec in (oracle.fastssc_decode, oracle.sc_decode):
+        xh = dec(frozen, llr)
+        assert not oracle.encode(xh)[:, frozen == 1].any()
+    clean = (1.0 - 2.0 * x).astype(np.float32) * 8.0
+    if i8:
+        clean = si.quantize_i8(clean)
+    for dec in (oracle.fastssc_decode, oracle.sc_decode):
+        xh = dec(frozen, clean)
+        assert np.array_equal(xh, x)
+        assert np.array_equal(oracle.info_bits(frozen, xh), bits)
+
+
+def test_int8_minus128_is_clamped():
+    """-128 is outside the symmetric range (reading C8): decoded as -127."""
+    frozen = oracle.construct_ga(64, 32, 2.0)
+    a = si.random_llr_i8(3, (40, 64))
+    a[:, ::3] = -128
+    b = a.copy(); b[b == -128] = -127
+    assert np.array_equal(oracle.fastssc_decode(frozen, a), oracle.fastssc_decode(frozen, b))
+    assert np.array_equal(oracle.sc_decode(frozen, a), oracle.sc_decode(frozen, b))
+
+
+def test_pack_unpack_roundtrip():
+    rng = np.random.default_rng(0)
+    b = rng.integers(0, 2, (5, 77), dtype=np.uint8)
+    w = oracle.pack_bits(b)
+    assert w.shape == (5, 3) and w.dtype == np.uint32
+    assert np.array_equal(oracle.unpack_bits(w, 77), b)
+    assert int(oracle.pack_bits(np.array([[1, 0, 1]], np.uint8))[0, 0]) == 5
+
+
+# ------------------------------------------------------------------ construction
+def test_bhattacharyya_closed_forms():
+    """BEC(z0): the all-minus channel has z = 1 - (1 - z0)^N and the all-plus z0^N."""
+    z = oracle.bhattacharyya_bec(8, 0.5)
+    assert z[0] == pytest.approx(1 - 0.5 ** 8)
+    assert z[7] == pytest.approx(0.5 ** 8)
+    # capacity is conserved on the BEC: sum of (1 - z_i) = N (1 - z0)
+    for N in (8, 64, 1024):
+        assert np.sum(1 - oracle.bhattacharyya_bec(N, 0.3)) == pytest.approx(N * 0.7)
+
+
+def test_ga_ordering_n8_matches_bhattacharyya():
+    """For N = 8 the GA ranks bit channels 0,1,2,4,3,5,6,7 (least reliable first) at every
+    design SNR from -3 to 10 dB, the same order as the textbook BEC(0.5) recursion
+    (SURVEY 0.1 fact 3).  Hence no reliability construction yields P:187-194's {0,1,4}."""
+    zorder = list(np.argsort(-oracle.bhattacharyya_bec(8, 0.5), kind="stable"))
+    assert zorder == [0, 1, 2, 4, 3, 5, 6, 7]
+    for snr in np.arange(-3.0, 10.5, 0.5):
+        m = oracle.ga_means(8, 4, float(snr))
+        assert list(np.argsort(m, kind="stable")) == zorder
+        assert set(np.flatnonzero(oracle.construct_ga(8, 5, float(snr)))) == {0, 1, 2}
+
+
+@pytest.mark.parametrize("N,K,ebn0", [(64, 32, 1.0), (1024, 512, 2.5), (2048, 1723, 4.0), (32768, 29492, 4.5)])
+def test_ga_respects_bit_dominance(N, K, ebn0):
+    """Universal partial order: if the bits of i are a subset of the bits of j, channel j is
+    at least as reliable (a theorem for any symmetric channel).  So the GA means are
+    monotone under bit dominance and the information set is superset-closed."""
+    m = oracle.ga_means(N, K, ebn0)
+    n = N.bit_length() - 1
+    for b in range(n):
+        i = np.arange(N)
+        lo = i[(i >> b) & 1 == 0]
+        assert np.all(m[lo | (1 << b)] >= m[lo] * (1 - 1e-12))
+    frozen = oracle.construct_ga(N, K, ebn0)
+    assert frozen.sum() == N - K
+    info = np.flatnonzero(frozen == 0)
+    for b in range(n):
+        assert np.all(frozen[info | (1 << b)] == 0)
+
+
+def test_phi_inverse():
+    for x in (0.01, 0.5, 3.0, 9.9, 10.5, 40.0, 500.0, 1e5):
+        y = oracle.lib().or_log_phi(x)
+        assert oracle.lib().or_inv_log_phi(y) == pytest.approx(x, rel=1e-9)
+
+
+# Op counts of the unfused Listing-1 schedule for the GA masks (counts
+# obtained during the survey with the same GA recipe; a mismatch means a different mask).
+OP_COUNTS = [((1024, 512, 2.5), 299), ((2048, 1723, 4.0), 371),
+             ((32768, 29492, 4.5), 2607), ((32768, 27568, 4.0), 3577)]
+
+
+@pytest.mark.parametrize("code,ops", OP_COUNTS)
+def test_op_counts_match_survey(code, ops):
+    N, K, ebn0 = code
+    assert len(oracle.fastssc_trace(oracle.construct_ga(N, K, ebn0))) == ops
+
+
+# ------------------------------------------------------------------ statistics (weak pins)
+def _q(x):
+    from math import erfc, sqrt
+    return 0.5 * erfc(x / sqrt(2.0))
+
+
+@pytest.mark.slow
+def test_fer_close_to_ga_prediction_and_int8_loss_small():
+    """FER of (1024,512) at 2.5 dB vs the GA union/product estimate
+    1 - prod_{i in A} (1 - Q(sqrt(m_i / 2))) (SURVEY 8(c) pin 9, weak), and the 8-bit
+    profile costs little error-correction performance."""
+    N, K, ebn0, n = 1024, 512, 2.5, 3000
+    frozen, bits, x, llr = _frames(N, K, ebn0, n, 21)
+    m = oracle.ga_means(N, K, ebn0)
+    pred = 1.0 - np.prod([1.0 - _q(np.sqrt(m[i] / 2.0)) for i in np.flatnonzero(frozen == 0)])
+    fer = np.mean(np.any(oracle.fastssc_decode(frozen, llr) != x, axis=1))
+    assert 0.4 * pred < fer < 2.5 * pred
+    fer8 = np.mean(np.any(oracle.fastssc_decode(frozen, si.quantize_i8(llr)) != x, axis=1))
+    assert fer8 < 1.5 * fer + 10.0 / n
