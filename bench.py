@@ -1,0 +1,306 @@
+"""Benchmark of the B200 Fast-SSC polar decoder (the driver's bench contract).
+
+One step = one polar_decode_i8 call over a batch of B frames of the (32768,29492) code
+(BASELINE.json's metric code; int8 profile), LLRs resident in HBM (B*N bytes > L2, so no
+flush is needed).  value = information bits decoded per second over all ranks (Gbps).
+
+Also reported on the same line:
+  e2e            the same metric through polar_decode_i8_host (pinned host LLRs -> device ->
+                 host info bits, copies inside the timed region);
+  latency        batch-1 single-frame decode time (config 3), kernel-only (CUDA events);
+  roofline       the decode kernel against the ALU issue ceiling;
+  cpu_baseline   the CPU oracle (oracle/, plain C) on a bounded sample, rank 0 only;
+  extra          the (2048,1723) int8 throughput (config 2) and FER/BER of the timed frames.
+
+--impl reference times the CPU oracle instead (the reference arm of this tier).
+Multi-GPU: torchrun, one rank per GPU, frames sharded (weak scaling), NCCL all-reduce of
+the error counters and MAX of the elapsed time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 1504000353
+CODE = (32768, 29492, 4.5)       # config 3/5 code, design = operating Eb/N0 (reading C1)
+CODE2 = (2048, 1723, 4.0)        # config 2 code
+BATCH = 16384                    # frames per step per GPU for N=32768 (512 MiB of int8 LLRs)
+BATCH2 = 1 << 20                 # frames per step per GPU for N=2048 (2 GiB)
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """Samples nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._p = index, [], None
+
+    def __enter__(self):
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "100"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self._p = None
+        return self
+
+    def _read(self):
+        for line in self._p.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) == 6:
+                self.rows.append(f)
+
+    def __exit__(self, *a):
+        if self._p:
+            time.sleep(0.15)
+            self._p.terminate()
+            self._p.wait()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_oracle_rate(N, K, e, sample_frames, threads, seconds_cap=20.0):
+    """Oracle O2 (plain C Fast-SSC) on host cores: info bits/s over a bounded sample."""
+    import oracle
+    from seeded_inputs import bpsk_awgn_llr, draw, quantize_i8
+
+    mask = oracle.construct_ga(N, K, e)
+    base = 64
+    bits, noise = draw(SEED, 0, base, K, N)
+    q = quantize_i8(bpsk_awgn_llr(oracle.encode_systematic(mask, bits), noise, e, K))
+    reps = max(1, sample_frames // base)
+    llr = np.ascontiguousarray(np.tile(q, (reps, 1)))
+    t0 = time.perf_counter()
+    oracle.fastssc_decode(mask, llr, threads=threads)
+    dt = time.perf_counter() - t0
+    n = llr.shape[0]
+    return n * K / dt, n, dt
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    N, K, e = CODE
+    cores = os.cpu_count() or 1
+    samples = []
+    for _ in range(args.warmup):
+        cpu_oracle_rate(N, K, e, 256, cores)
+    for _ in range(args.steps):
+        r, n, dt = cpu_oracle_rate(N, K, e, 512, cores)
+        samples.append((r, n, dt))
+    rate = sum(s[1] for s in samples) * K / sum(s[2] for s in samples)
+    v = rate / 1e9
+    ms = 1e3 * float(np.mean([s[2] for s in samples]))
+    line = {"impl": "reference", "metric": "info_gbps", "value": v, "unit": "Gbps", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+            "config": {"workload": f"({N},{K}) int8 Fast-SSC, CPU oracle, 512-frame sample per step",
+                       "code": [N, K], "ebn0_db": e, "global_batch": 512, "parallelism": "host threads"},
+            "cpu_baseline": {"value": v, "unit": "Gbps", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} x 512 frames of ({N},{K}) int8 (64 seeded AWGN frames tiled)"},
+            "e2e": {"value": v, "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--no-extra", action="store_true", help="skip the (2048,1723) and latency legs")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1504_00353_b200 as pb
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(t):
+        if ws > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return t
+
+    def throughput(code_t, B, steps, warmup, with_e2e):
+        N, K, e = code_t
+        code = pb.PolarCode.ga(N, K, e)
+        llr = torch.empty(B, N, dtype=torch.int8, device=dev)
+        truth = torch.empty(B, code.info_words, dtype=torch.int32, device=dev)
+        out = torch.empty(B, code.info_words, dtype=torch.int32, device=dev)
+        code.gen_bpsk_awgn(SEED, rank * B, B, e, 4.0, llr_i8=llr, info=truth)
+        stream = torch.cuda.current_stream()
+        for _ in range(warmup):
+            code.decode_i8(llr, out)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        with Clocks(local) as clk:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record(stream)
+            for i in range(steps):
+                ev[i][0].record(stream)
+                code.decode_i8(llr, out)
+                ev[i][1].record(stream)
+            t1.record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        total_ms = max_over_ranks(t0.elapsed_time(t1))
+        per_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        ctr = torch.zeros(3, dtype=torch.int64, device=dev)
+        code.count_errors(out, truth, ctr)
+        sum_over_ranks(ctr)
+        frames, bit_err, frame_err = ctr.tolist()
+        res = {"code": code, "N": N, "K": K, "B": B, "total_ms": total_ms, "ms_per_step": total_ms / steps,
+               "launch_ms": per_launch_ms, "gbps": ws * B * K * steps / (total_ms * 1e-3) / 1e9,
+               "fer": frame_err / max(frames, 1), "ber": bit_err / max(frames * K, 1), "clocks": clk.summary()}
+        if with_e2e:
+            host = llr.cpu().pin_memory()
+            hout = torch.empty(B, code.info_words, dtype=torch.int32).pin_memory()
+            code.decode_host(host, hout)
+            barrier()
+            e2e_steps = max(1, min(steps, 5))
+            t = time.perf_counter()
+            for _ in range(e2e_steps):
+                code.decode_host(host, hout)
+            dt = max_over_ranks(time.perf_counter() - t)
+            assert torch.equal(hout, out.cpu()), "host path disagrees with the device path"
+            res["e2e"] = {"value": ws * B * K * e2e_steps / dt / 1e9, "unit": "Gbps",
+                          "h2d_bytes_per_step": B * N, "d2h_bytes_per_step": B * code.info_words * 4}
+            del host, hout
+        del llr, truth, out
+        torch.cuda.empty_cache()
+        return res
+
+    def latency_batch1(code_t, iters=300):
+        N, K, e = code_t
+        code = pb.PolarCode.ga(N, K, e)
+        llr = torch.empty(1, N, dtype=torch.int8, device=dev)
+        out = torch.empty(1, code.info_words, dtype=torch.int32, device=dev)
+        llr32 = torch.empty(1, N, dtype=torch.float32, device=dev)
+        code.gen_bpsk_awgn(SEED, 0, 1, e, 4.0, llr_f32=llr32, llr_i8=llr)
+        stream = torch.cuda.current_stream()
+        res = {}
+        for prof, x, fn in (("i8", llr, code.decode_i8), ("f32", llr32, code.decode_f32)):
+            for _ in range(20):
+                fn(x, out)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(iters):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                fn(x, out)
+                b.record(stream)
+                ts.append((a, b))
+            torch.cuda.synchronize()
+            us = np.array([a.elapsed_time(b) * 1e3 for a, b in ts])
+            res[prof] = {"p50_us": float(np.median(us)), "p99_us": float(np.percentile(us, 99))}
+        res["n_ops"] = code.n_ops
+        return res
+
+    main_r = throughput(CODE, args.batch, args.steps, args.warmup, with_e2e=True)
+    extra = {}
+    if not args.no_extra:
+        r2 = throughput(CODE2, BATCH2, max(3, args.steps // 2), args.warmup, with_e2e=False)
+        extra["c2048_1723_i8"] = {"info_gbps": r2["gbps"], "frames_per_s": ws * r2["B"] / (r2["ms_per_step"] * 1e-3),
+                                  "batch_per_gpu": r2["B"], "ms_per_step": r2["ms_per_step"], "fer": r2["fer"]}
+        extra["latency_batch1_32768_29492"] = latency_batch1(CODE)
+        extra["latency_batch1_2048_1723"] = latency_batch1(CODE2)
+    N, K = main_r["N"], main_r["K"]
+    B = main_r["B"]
+    # Roofline: the decode kernel is ALU/issue bound.  Algorithmic work
+    # = elementary LLR operations per frame (f, g, leaf elements) x frames; peak = one lane-op
+    # per lane per clock on every SM at the max SM clock.
+    elem = {29492: 104500 + 106042 + 31226}[K]
+    sm_mhz = 1965.0
+    peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # T lane-ops/s
+    achieved = elem * B / (main_r["launch_ms"] * 1e-3) / 1e12
+    hbm_bytes = B * (N + 4 * code_words(K))
+    line = {
+        "metric": "info_gbps", "value": main_r["gbps"], "unit": "Gbps", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": main_r["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": {"workload": f"({N},{K}) systematic polar, int8 Fast-SSC, BPSK-AWGN {CODE[2]} dB, "
+                               f"{B} frames/GPU per step resident in HBM",
+                   "code": [N, K], "ebn0_db": CODE[2], "global_batch": B * ws, "batch_per_gpu": B,
+                   "l2_flush": "inputs larger than L2 (512 MiB int8 LLRs per GPU)", "parallelism": f"dp{ws}"},
+        "e2e": main_r["e2e"],
+        "gpu_launches": args.steps,
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (lane-ops)",
+                     "frac": achieved / peak, "traffic": None,
+                     "hbm_achieved_gbs": hbm_bytes / (main_r["launch_ms"] * 1e-3) / 1e9,
+                     "hbm_frac_of_measured": hbm_bytes / (main_r["launch_ms"] * 1e-3) / 1e9 / 6554.6},
+        "clocks": main_r["clocks"],
+        "fer": main_r["fer"], "ber": main_r["ber"],
+        "extra": extra,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        r, n, dt = cpu_oracle_rate(N, K, CODE[2], 1024, cores)
+        line["cpu_baseline"] = {"value": r / 1e9, "unit": "Gbps", "cores": cores, "kind": "oracle",
+                                "sample": f"{n} frames of ({N},{K}) int8 (64 seeded AWGN frames tiled), {dt:.1f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def code_words(K):
+    return (K + 31) // 32
+
+
+if __name__ == "__main__":
+    main()

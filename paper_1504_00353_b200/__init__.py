@@ -1,0 +1,210 @@
+"""B200-native Fast-SSC polar decoding (Giard et al., arXiv:1504.00353).
+
+Thin ctypes binding over ``libpolar.so`` (C ABI declared in ``include/polar.h``): argument
+marshalling only.  Every step of the decode runs in the library's sm_100a kernels; torch is
+used for device memory and streams.  There is no CPU fallback: if the library is missing
+the import of ``lib()`` raises, and without a GPU every device call raises ``PolarError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpolar.so")
+
+POLAR_OK = 0
+POLAR_ERR_INVALID_ARGUMENT = 1
+POLAR_ERR_UNSUPPORTED_CODE = 2
+POLAR_ERR_CUDA = 3
+POLAR_ERR_OUT_OF_MEMORY = 4
+
+# Every symbol include/polar.h declares (checked by tests/test_abi.py).
+EXPORTS = [
+    "polar_status_string", "polar_last_error", "polar_code_create", "polar_code_destroy",
+    "polar_code_query", "polar_code_schedule", "polar_code_mask", "polar_decode_f32",
+    "polar_decode_i8", "polar_decode_f32_host", "polar_decode_i8_host", "polar_construct_ga",
+    "polar_encode_systematic", "polar_gen_bpsk_awgn", "polar_count_errors",
+    "polar_registry_size", "polar_registry_entry",
+]
+
+
+class PolarError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libpolar.so (built by ``build()``); raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run paper_1504_00353_b200.build.build() first")
+    L = C.CDLL(LIB_PATH)
+    vp, u8p, u32p, i64p = C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_int64)
+    sig = {
+        "polar_status_string": (C.c_char_p, [C.c_int]),
+        "polar_last_error": (C.c_char_p, []),
+        "polar_code_create": (C.c_int, [C.c_uint32, C.c_uint32, vp, C.POINTER(vp)]),
+        "polar_code_destroy": (None, [vp]),
+        "polar_code_query": (C.c_int, [vp, u32p, u32p, u32p, u32p, u32p]),
+        "polar_code_schedule": (C.c_int, [vp, C.c_char_p, C.c_uint32, u32p]),
+        "polar_code_mask": (C.c_int, [vp, vp]),
+        "polar_decode_f32": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
+        "polar_decode_i8": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
+        "polar_decode_f32_host": (C.c_int, [vp, vp, C.c_int64, vp]),
+        "polar_decode_i8_host": (C.c_int, [vp, vp, C.c_int64, vp]),
+        "polar_construct_ga": (C.c_int, [C.c_uint32, C.c_uint32, C.c_double, vp]),
+        "polar_encode_systematic": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
+        "polar_gen_bpsk_awgn": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_int64, C.c_double, C.c_float,
+                                          vp, vp, vp, vp]),
+        "polar_count_errors": (C.c_int, [vp, vp, vp, C.c_int64, vp, vp]),
+        "polar_registry_size": (C.c_uint32, []),
+        "polar_registry_entry": (C.c_int, [C.c_uint32, u32p, u32p, vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _ = (u8p, i64p)
+    _lib = L
+    return L
+
+
+def _check(status: int) -> None:
+    if status != POLAR_OK:
+        L = lib()
+        raise PolarError(status, f"{L.polar_status_string(status).decode()}: {L.polar_last_error().decode()}")
+
+
+def _ptr(t) -> int | None:
+    """Device/host address of a torch tensor or numpy array (None -> NULL)."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+def construct_ga(N: int, K: int, design_ebn0_db: float) -> np.ndarray:
+    """Frozen mask (uint8[N], 1 = frozen) of the GA construction (reading C1)."""
+    m = np.zeros(N, np.uint8)
+    _check(lib().polar_construct_ga(N, K, float(design_ebn0_db), m.ctypes.data))
+    return m
+
+
+def registry() -> list[tuple[int, int, np.ndarray]]:
+    """(N, K, frozen mask) of every code specialised into this build."""
+    L = lib()
+    out = []
+    for i in range(L.polar_registry_size()):
+        n, k = C.c_uint32(), C.c_uint32()
+        _check(L.polar_registry_entry(i, C.byref(n), C.byref(k), None))
+        m = np.zeros(n.value, np.uint8)
+        _check(L.polar_registry_entry(i, None, None, m.ctypes.data))
+        out.append((n.value, k.value, m))
+    return out
+
+
+class PolarCode:
+    """Handle of one (N, K, frozen set) code: ``polar_code_create`` / ``polar_code_destroy``."""
+
+    def __init__(self, N: int, K: int, frozen_mask: np.ndarray):
+        m = np.ascontiguousarray(np.asarray(frozen_mask, np.uint8))
+        if m.shape != (N,):
+            raise ValueError("frozen mask must have N entries")
+        h = C.c_void_p()
+        _check(lib().polar_code_create(N, K, m.ctypes.data, C.byref(h)))
+        self._h = h
+        n, k, ops, smem, wr = (C.c_uint32() for _ in range(5))
+        _check(lib().polar_code_query(h, C.byref(n), C.byref(k), C.byref(ops), C.byref(smem), C.byref(wr)))
+        self.N, self.K, self.n_ops, self.smem_bytes, self.warp_root = n.value, k.value, ops.value, smem.value, wr.value
+        self.info_words = (self.K + 31) // 32
+
+    @classmethod
+    def ga(cls, N: int, K: int, design_ebn0_db: float) -> "PolarCode":
+        return cls(N, K, construct_ga(N, K, design_ebn0_db))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().polar_code_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def mask(self) -> np.ndarray:
+        m = np.zeros(self.N, np.uint8)
+        _check(lib().polar_code_mask(self._h, m.ctypes.data))
+        return m
+
+    def schedule(self) -> list[str]:
+        need = C.c_uint32()
+        _check(lib().polar_code_schedule(self._h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        _check(lib().polar_code_schedule(self._h, buf, need.value, None))
+        return [s for s in buf.value.decode().split(";") if s]
+
+    # ----------------------------------------------------------------- hot path
+    def _out(self, n: int, out, device):
+        if out is None:
+            import torch
+            out = torch.empty((n, self.info_words), dtype=torch.int32, device=device)
+        return out
+
+    def decode_f32(self, llr, out=None, stream=None):
+        """Fast-SSC decode of float32 LLRs [n, N] (device) -> packed info bits [n, ceil(K/32)]."""
+        n = llr.shape[0] if llr.dim() > 1 else llr.numel() // self.N
+        out = self._out(n, out, llr.device)
+        _check(lib().polar_decode_f32(self._h, _ptr(llr), n, _ptr(out), _stream(stream)))
+        return out
+
+    def decode_i8(self, llr, out=None, stream=None):
+        """Fast-SSC decode of int8 LLRs [n, N] (device) -> packed info bits [n, ceil(K/32)]."""
+        n = llr.shape[0] if llr.dim() > 1 else llr.numel() // self.N
+        out = self._out(n, out, llr.device)
+        _check(lib().polar_decode_i8(self._h, _ptr(llr), n, _ptr(out), _stream(stream)))
+        return out
+
+    def decode_host(self, llr, out):
+        """End-to-end decode of HOST LLRs (float32 or int8 [n, N]) into HOST out [n, words]."""
+        is_i8 = str(llr.dtype).endswith("int8")
+        n = llr.shape[0]
+        fn = lib().polar_decode_i8_host if is_i8 else lib().polar_decode_f32_host
+        _check(fn(self._h, _ptr(llr), n, _ptr(out)))
+        return out
+
+    # ----------------------------------------------------------------- non-hot helpers
+    def encode_systematic(self, info, out=None, stream=None):
+        import torch
+        n = info.shape[0]
+        if out is None:
+            out = torch.empty((n, max(1, self.N // 32)), dtype=torch.int32, device=info.device)
+        _check(lib().polar_encode_systematic(self._h, _ptr(info), n, _ptr(out), _stream(stream)))
+        return out
+
+    def gen_bpsk_awgn(self, seed: int, first_frame: int, n: int, ebn0_db: float, q_scale: float = 4.0,
+                      llr_f32=None, llr_i8=None, info=None, stream=None):
+        _check(lib().polar_gen_bpsk_awgn(self._h, seed, first_frame, n, float(ebn0_db), float(q_scale),
+                                         _ptr(llr_f32), _ptr(llr_i8), _ptr(info), _stream(stream)))
+
+    def count_errors(self, decoded, truth, counters, stream=None):
+        n = decoded.shape[0]
+        _check(lib().polar_count_errors(self._h, _ptr(decoded), _ptr(truth), n, _ptr(counters), _stream(stream)))

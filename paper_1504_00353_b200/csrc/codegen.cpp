@@ -1,0 +1,354 @@
+// codegen.cpp -- build-time emitter of the unrolled Fast-SSC decoders (product code).
+//
+// The paper's unrolled decoders are generated per code as a straight list of function calls
+// with compile-time sizes (Listing 1; "the decoder ... is generated", P:641;
+// template sizes and unrolled loops).  This program does the same for SIMT:
+// for every code listed in the spec file it walks the Fast-SSC tree (tree.hpp) depth first
+// and writes build/gen/code_<name>.cu, a sequence of calls to the device templates of
+// decoder.cuh with every size, register stage and bit offset a compile-time constant, and
+// the registry (build/gen/registry.cpp) that polar_code_create searches.
+//
+// Spec file lines:  <name> <N> <K> ga <design Eb/N0 dB> [W=<warp root>] [T=<threads>]
+//                   <name> <N> <K> mask <N characters 0/1, 1 = frozen>   [...]
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "tree.hpp"
+
+namespace polar {
+void construct_ga(int N, int K, double design_ebn0_db, uint8_t* frozen);
+}
+
+using namespace polar;
+
+namespace {
+
+int ilog2(int n) {
+    int k = 0;
+    while ((1 << k) < n) ++k;
+    return k;
+}
+
+struct Spec {
+    std::string name;
+    int N = 0, K = 0;
+    std::vector<uint8_t> mask;
+    int W = 1024;   // warp subtree size for CTA mode
+    int T = 512;    // threads per CTA in CTA mode
+    int warps = 4;  // frames (warps) per CTA in warp mode
+};
+
+struct Emitter {
+    const Tree& t;
+    std::ostringstream& o;
+    int next_mask = 0;
+    std::string ind = "        ";
+
+    std::string mask_name() { return "m" + std::to_string(next_mask++); }
+
+    // Emit the warp-scope decode of node id (size n) at bit offset off relative to the
+    // subtree root.  src: the C++ expression of its LLR source.  Returns the name of the
+    // uniform mask holding its beta when n <= 32, "" when beta was written into bw.
+    std::string warp(int id, int off, const std::string& src) {
+        const Node& v = t.nodes[id];
+        const int n = v.n;
+        const int s0 = off / 32;
+        const std::string N_ = std::to_string(n), S0 = std::to_string(s0);
+        switch (v.kind) {
+            case Kind::Rate0:
+                return n <= 32 ? "0u" : "";
+            case Kind::Rate1:
+                if (n <= 32) {
+                    std::string m = mask_name();
+                    o << ind << "const uint32_t " << m << " = wR1m<P, " << N_ << ">(" << src << ");\n";
+                    return m;
+                }
+                o << ind << "wR1<P, " << N_ << ", " << S0 << ">(" << src << ", bw);\n";
+                return "";
+            case Kind::Rep:
+                if (n <= 32) {
+                    std::string m = mask_name();
+                    o << ind << "const uint32_t " << m << " = wRepm<P, " << N_ << ">(" << src << ");\n";
+                    return m;
+                }
+                o << ind << "wRep<P, " << N_ << ", " << S0 << ">(" << src << ", bw);\n";
+                return "";
+            case Kind::Spc:
+                if (n <= 32) {
+                    std::string m = mask_name();
+                    o << ind << "const uint32_t " << m << " = wSPCm<P, " << N_ << ">(" << src << ");\n";
+                    return m;
+                }
+                o << ind << "wSPC<P, " << N_ << ", " << S0 << ">(" << src << ", bw);\n";
+                return "";
+            case Kind::Split:
+                break;
+        }
+        const int h = n / 2;
+        const std::string H = std::to_string(h);
+        const std::string child = "r" + std::to_string(ilog2(h));
+        const std::string csrc = "RegSrc<P>{" + child + "}";
+        const Node& l = t.nodes[v.left];
+        const Node& r = t.nodes[v.right];
+        if (l.kind == Kind::Rate0) {
+            o << ind << "wG0R<P, " << N_ << ">(" << src << ", " << child << ");\n";
+            std::string mr = warp(v.right, off + h, csrc);
+            if (n <= 32) {
+                std::string m = mask_name();
+                o << ind << "const uint32_t " << m << " = " << mr << " | (" << mr << " << " << H << ");\n";
+                return m;
+            }
+            if (h == 32 && mr != "0u") o << ind << "wDeposit<" << (off + h) / 32 << ">(bw, " << mr << ");\n";
+            o << ind << "wComb0R<" << N_ << ", " << S0 << ">(bw);\n";
+            return "";
+        }
+        o << ind << "wF<P, " << N_ << ">(" << src << ", " << child << ");\n";
+        std::string ml = warp(v.left, off, csrc);
+        if (h == 32 && ml != "0u") o << ind << "wDeposit<" << s0 << ">(bw, " << ml << ");\n";
+        if (r.kind == Kind::Rate0) return n <= 32 ? ml : "";
+        o << ind << "wG<P, " << N_ << ", " << S0 << ">(" << src << ", " << child << ", bw, "
+          << (n <= 32 ? ml : std::string("0u")) << ");\n";
+        std::string mr = warp(v.right, off + h, csrc);
+        if (n <= 32) {
+            std::string m = mask_name();
+            o << ind << "const uint32_t " << m << " = (" << ml << " ^ " << mr << ") | (" << mr << " << " << H
+              << ");\n";
+            return m;
+        }
+        if (h == 32 && mr != "0u") o << ind << "wDeposit<" << (off + h) / 32 << ">(bw, " << mr << ");\n";
+        o << ind << "wComb<" << N_ << ", " << S0 << ">(bw);\n";
+        return "";
+    }
+};
+
+// A warp subtree function: root node id, whose input LLRs are at `src` (shared memory).
+void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::string& fname) {
+    const Node& v = t.nodes[id];
+    const int R = v.n;
+    o << "    template <class P, class SrcT>\n"
+      << "    static PD_INLINE void " << fname << "(const SrcT* src_ptr, uint32_t* beta) {\n"
+      << "        using V = typename P::v_t;\n"
+      << "        const MemSrc<P, SrcT> src{src_ptr};\n";
+    for (int k = ilog2(R) - 1; k >= 0; --k) {
+        const int size = 1 << k;
+        o << "        V r" << k << "[" << (size >= 32 ? size / 32 : 1) << "];\n";
+    }
+    o << "        uint64_t bw = 0;\n        (void)bw;\n";
+    Emitter e{t, o};
+    std::string m = e.warp(id, 0, "src");
+    if (R >= 64) {
+        o << "        wStoreBeta<" << R << ">(bw, beta + " << v.off / 32 << ");\n";
+    } else {
+        // R <= 32 only when the whole frame is this subtree (N <= 32): word 0.
+        o << "        if (lane_id() == 0) beta[" << v.off / 32 << "] = " << m << ";\n";
+    }
+    o << "    }\n";
+}
+
+struct CtaEmitter {
+    const Tree& t;
+    std::ostringstream& body;   // decode_cta body
+    std::ostringstream& subs;   // warp subtree functions
+    int W, T, N;
+    std::map<int, int> stage_off;  // stage size -> element offset
+    int n_subs = 0;
+
+    std::string stage(int m) { return "(stages + " + std::to_string(stage_off.at(m)) + ")"; }
+
+    void sub_call(int id, const std::string& src) {
+        std::string fname = "sub" + std::to_string(n_subs++);
+        emit_warp_sub(subs, t, id, fname);
+        body << "        if (threadIdx.x < 32) " << fname << "<P>(" << src << ", beta);\n"
+             << "        __syncthreads();\n";
+    }
+
+    void child(int id, const std::string& src) {
+        const Node& v = t.nodes[id];
+        if (v.kind == Kind::Rate0) return;  // beta zeroed at frame start
+        if (v.n > W) cta(id, src);
+        else sub_call(id, src);
+    }
+
+    void cta(int id, const std::string& src) {
+        const Node& v = t.nodes[id];
+        const int n = v.n;
+        const std::string N_ = std::to_string(n);
+        const std::string B = "(beta + " + std::to_string(v.off / 32) + ")";
+        switch (v.kind) {
+            case Kind::Rate0:
+                return;
+            case Kind::Rate1:
+                body << "        cR1<P, T, " << N_ << ">(" << src << ", " << B << ");\n        __syncthreads();\n";
+                return;
+            case Kind::Rep:
+                body << "        cRep<P, T, " << N_ << ">(" << src << ", " << stage(n / 2) << ", " << B
+                     << ");\n        __syncthreads();\n";
+                return;
+            case Kind::Spc:
+                body << "        cSPC<P, T, " << N_ << ">(" << src << ", " << B << ");\n        __syncthreads();\n";
+                return;
+            case Kind::Split:
+                break;
+        }
+        const int h = n / 2;
+        const std::string D = stage(h);
+        const Node& l = t.nodes[v.left];
+        const Node& r = t.nodes[v.right];
+        if (l.kind == Kind::Rate0) {
+            body << "        cG0R<P, T, " << N_ << ">(" << src << ", " << D << ");\n        __syncthreads();\n";
+            child(v.right, D);
+            body << "        cComb0R<T, " << N_ << ">(" << B << ");\n        __syncthreads();\n";
+            return;
+        }
+        body << "        cF<P, T, " << N_ << ">(" << src << ", " << D << ");\n        __syncthreads();\n";
+        child(v.left, D);
+        if (r.kind == Kind::Rate0) return;
+        body << "        cG<P, T, " << N_ << ">(" << src << ", " << D << ", " << B << ");\n        __syncthreads();\n";
+        child(v.right, D);
+        body << "        cComb<T, " << N_ << ">(" << B << ");\n        __syncthreads();\n";
+    }
+};
+
+std::string mask_string(const std::vector<uint8_t>& m) {
+    std::string s;
+    for (uint8_t b : m) s += b ? '1' : '0';
+    return s;
+}
+
+void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& reg_decl,
+               std::ostringstream& reg_entries) {
+    Tree t = build_tree(sp.N, sp.mask.data());
+    std::vector<std::string> ops = schedule(t);
+    const bool warp_mode = sp.N <= 2048;
+    std::ostringstream o;
+    o << "// Generated by codegen.cpp for code " << sp.name << " (N=" << sp.N << ", K=" << sp.K
+      << ", " << ops.size() << " Fast-SSC ops). Do not edit.\n"
+      << "#include \"kernels.cuh\"\n\nnamespace pd {\nnamespace code_" << sp.name << " {\n\n"
+      << "struct Code {\n"
+      << "    static constexpr int N = " << sp.N << ";\n"
+      << "    static constexpr int K = " << sp.K << ";\n";
+    if (warp_mode) {
+        o << "    static constexpr int WARPS = " << sp.warps << ";\n"
+          << "    static constexpr int MIN_BLOCKS = 1;\n";
+        emit_warp_sub(o, t, 0, "decode_root");
+        o << "    template <class P>\n"
+          << "    static PD_INLINE void decode_warp(const typename P::in_t* chan, uint32_t* beta) {\n"
+          << "        decode_root<P>(chan, beta);\n    }\n";
+    } else {
+        std::ostringstream body, subs;
+        CtaEmitter ce{t, body, subs, sp.W, sp.T, sp.N, {}, 0};
+        int acc = 0;
+        for (int m = sp.N / 2; m >= sp.W; m /= 2) {
+            ce.stage_off[m] = acc;
+            acc += m;
+        }
+        ce.cta(0, "chan");
+        o << "    static constexpr int T = " << sp.T << ";\n"
+          << "    static constexpr int W = " << sp.W << ";\n"
+          << "    static constexpr int STAGE_ELEMS = " << acc << ";\n";
+        o << subs.str();
+        o << "    template <class P, class ChanT>\n"
+          << "    static PD_INLINE void decode_cta(const ChanT* chan, typename P::st_t* stages, uint32_t* beta) {\n"
+          << body.str() << "    }\n";
+    }
+    o << "};\n\n}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
+    const std::string kern = warp_mode ? "k_warp" : "k_cta";
+    const std::string lay = warp_mode ? "WarpLayout" : "CtaLayout";
+    const std::string C = "pd::code_" + sp.name + "::Code";
+    o << "extern const void* const polar_kern_" << sp.name << "_f32 = (const void*)&pd::" << kern
+      << "<pd::PF32, " << C << ">;\n"
+      << "extern const void* const polar_kern_" << sp.name << "_i8 = (const void*)&pd::" << kern
+      << "<pd::PI8, " << C << ">;\n"
+      << "extern const unsigned polar_smem_" << sp.name << "_f32 = pd::" << lay << "<pd::PF32, " << C
+      << ">::SMEM;\n"
+      << "extern const unsigned polar_smem_" << sp.name << "_i8 = pd::" << lay << "<pd::PI8, " << C
+      << ">::SMEM;\n";
+    std::ofstream(outdir + "/code_" + sp.name + ".cu") << o.str();
+
+    std::string sched;
+    for (auto& s : ops) sched += s + ";";
+    reg_decl << "extern const void* const polar_kern_" << sp.name << "_f32;\n"
+             << "extern const void* const polar_kern_" << sp.name << "_i8;\n"
+             << "extern const unsigned polar_smem_" << sp.name << "_f32;\n"
+             << "extern const unsigned polar_smem_" << sp.name << "_i8;\n"
+             << "static const uint8_t mask_" << sp.name << "[" << sp.N << "] = {";
+    for (int i = 0; i < sp.N; ++i) reg_decl << (i ? "," : "") << int(sp.mask[i]);
+    reg_decl << "};\n";
+    reg_entries << "    {\"" << sp.name << "\", " << sp.N << ", " << sp.K << ", mask_" << sp.name << ", "
+                << code_hash(sp.N, sp.K, sp.mask.data()) << "ull, " << ops.size() << ", "
+                << (warp_mode ? "MODE_WARP" : "MODE_CTA") << ", " << (warp_mode ? sp.N : sp.W) << ", "
+                << (warp_mode ? sp.warps * 32 : sp.T) << ", &polar_kern_" << sp.name << "_f32, &polar_kern_"
+                << sp.name << "_i8, &polar_smem_" << sp.name << "_f32, &polar_smem_" << sp.name << "_i8, "
+                << (warp_mode ? sp.warps : 1) << ", \"" << sched << "\"},\n";
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc != 3) {
+        std::cerr << "usage: polar_codegen <spec file> <output dir>\n";
+        return 1;
+    }
+    std::ifstream in(argv[1]);
+    if (!in) {
+        std::cerr << "codegen: cannot read " << argv[1] << "\n";
+        return 1;
+    }
+    std::vector<Spec> specs;
+    std::string line;
+    while (std::getline(in, line)) {
+        auto hash = line.find('#');
+        if (hash != std::string::npos) line = line.substr(0, hash);
+        std::istringstream ls(line);
+        Spec sp;
+        std::string how;
+        if (!(ls >> sp.name >> sp.N >> sp.K >> how)) continue;
+        if (sp.N < 2 || (sp.N & (sp.N - 1)) || sp.N > 32768 || sp.K < 1 || sp.K > sp.N) {
+            std::cerr << "codegen: bad (N, K) for " << sp.name << "\n";
+            return 2;
+        }
+        sp.mask.assign(sp.N, 0);
+        if (how == "ga") {
+            double ebn0;
+            ls >> ebn0;
+            construct_ga(sp.N, sp.K, ebn0, sp.mask.data());
+        } else if (how == "mask") {
+            std::string bits;
+            ls >> bits;
+            if ((int)bits.size() != sp.N) {
+                std::cerr << "codegen: mask length of " << sp.name << "\n";
+                return 2;
+            }
+            int nf = 0;
+            for (int i = 0; i < sp.N; ++i) nf += (sp.mask[i] = bits[i] == '1');
+            if (nf != sp.N - sp.K) {
+                std::cerr << "codegen: mask of " << sp.name << " has " << nf << " frozen bits\n";
+                return 2;
+            }
+        } else {
+            std::cerr << "codegen: unknown construction " << how << "\n";
+            return 2;
+        }
+        std::string opt;
+        while (ls >> opt) {
+            if (opt.rfind("W=", 0) == 0) sp.W = std::atoi(opt.c_str() + 2);
+            else if (opt.rfind("T=", 0) == 0) sp.T = std::atoi(opt.c_str() + 2);
+            else if (opt.rfind("WARPS=", 0) == 0) sp.warps = std::atoi(opt.c_str() + 6);
+        }
+        specs.push_back(sp);
+    }
+    std::ostringstream decl, entries;
+    for (auto& sp : specs) emit_code(sp, argv[2], decl, entries);
+    std::ostringstream reg;
+    reg << "// Generated by codegen.cpp. Do not edit.\n#include \"registry.hpp\"\n\n" << decl.str()
+        << "\nnamespace polar {\nconst RegistryEntry kRegistry[] = {\n" << entries.str() << "};\n"
+        << "const uint32_t kRegistrySize = " << specs.size() << ";\n}  // namespace polar\n";
+    std::ofstream(std::string(argv[2]) + "/registry.cpp") << reg.str();
+    return 0;
+}

@@ -1,0 +1,456 @@
+// decoder.cuh -- sm_100a device building blocks of the unrolled Fast-SSC decoders.
+//
+// Giard et al., arXiv:1504.00353.  The unrolled decoder is a straight list of operations
+// with compile-time sizes (Listing 1; template specialisation P:792-795).  Here
+// every operation is a force-inlined template instantiated by the code emitted per code
+// (codegen.cpp), re-derived for SIMT:
+//
+//  * warp scope (node sizes N_v <= W, W <= 2048): one warp owns the subtree.  The LLRs of
+//    the level-k stage (2^k values, the paper's alpha layout, one buffer per level,
+//    P:789-790) live in registers r_k[] with element i = lane + 32*slot.  F/G at N_v >= 64
+//    pair slot j with slot j + N_v/64 inside each lane; at N_v <= 32 the partner is
+//    N_v/2 lanes away (one shuffle).  The hard decisions beta of nodes with N_v >= 32 live
+//    as bits of a per-lane 64-bit word bw (bit s of lane l = beta[l + 32 s]); nodes with
+//    N_v <= 32 keep beta as a warp-uniform mask (bit i = beta[i]).  Combine (eq:combine
+//    P:318-325) is then a shift-and-xor on bw or on masks.
+//  * CTA scope (N_v > W, only for N > 2048): all threads of the CTA run the op on shared
+//    memory stages; beta is the codeword's natural bit array, packed in 32-bit words
+//    (one N-bit array, combined in place).
+//
+// Profiles (the paper's float and 8-bit fixed point):
+//  * PF32: f32 values; g is one IEEE add (__fadd_rn, no FMA contraction, reading C17);
+//  * PI8 : int8 storage, int32 registers; g saturates to [-127, 127] (reading C8).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pd {
+
+#define PD_INLINE __device__ __forceinline__
+constexpr unsigned FULL = 0xffffffffu;
+
+PD_INLINE unsigned lane_id() { return threadIdx.x & 31u; }
+
+__host__ __device__ constexpr int slots(int n) { return n >= 32 ? n / 32 : 1; }
+__host__ __device__ constexpr uint32_t low_mask(int n) { return n >= 32 ? 0xffffffffu : ((1u << n) - 1u); }
+
+// ------------------------------------------------------------------------------ profiles
+
+struct PF32 {
+    using in_t = float;   // channel LLR storage
+    using st_t = float;   // shared-memory stage storage (CTA scope)
+    using v_t = float;    // register value
+    using acc_t = float;  // repetition accumulator
+    static constexpr bool kExactSum = false;    // repetition sums in halving order (C13)
+    static constexpr bool kChanInSmem = false;  // N=32768 f32 channel does not fit with the tree
+    static PD_INLINE v_t ld(float x) { return x; }
+    static PD_INLINE float st(v_t x) { return x; }
+    // eq:f: sgn(a) sgn(b) min(|a|, |b|)
+    static PD_INLINE v_t f(v_t a, v_t b) {
+        const float m = fminf(fabsf(a), fabsf(b));
+        return __uint_as_float(__float_as_uint(m) | ((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u));
+    }
+    // eq:g: b + a if beta = 0 else b - a; beta flips the sign bit (P:817 idea)
+    static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) {
+        return __fadd_rn(b, __uint_as_float(__float_as_uint(a) ^ (beta << 31)));
+    }
+    static PD_INLINE v_t g0(v_t a, v_t b) { return __fadd_rn(b, a); }
+    static PD_INLINE bool hd(v_t a) { return a < 0.0f; }  // eq:info P:444-449, -0 -> 0 (C9)
+    static PD_INLINE uint32_t mag_key(v_t a) { return __float_as_uint(a) & 0x7fffffffu; }
+    static PD_INLINE acc_t acc(v_t a) { return a; }
+    static PD_INLINE acc_t add(acc_t a, acc_t b) { return __fadd_rn(a, b); }
+    static PD_INLINE bool acc_neg(acc_t a) { return a < 0.0f; }
+};
+
+struct PI8 {
+    using in_t = int8_t;
+    using st_t = int8_t;
+    using v_t = int;
+    using acc_t = int;
+    static constexpr bool kExactSum = true;
+    static constexpr bool kChanInSmem = true;
+    static PD_INLINE v_t ld(int8_t x) { return max((int)x, -127); }  // -128 -> -127 (C8)
+    static PD_INLINE int8_t st(v_t x) { return (int8_t)x; }
+    static PD_INLINE v_t f(v_t a, v_t b) {
+        const int m = min(abs(a), abs(b));
+        return (a ^ b) < 0 ? -m : m;
+    }
+    static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) {
+        const int s = beta ? b - a : b + a;
+        return min(max(s, -127), 127);  // saturating adder (max(-127) P:848)
+    }
+    static PD_INLINE v_t g0(v_t a, v_t b) { return min(max(b + a, -127), 127); }
+    static PD_INLINE bool hd(v_t a) { return a < 0; }
+    static PD_INLINE uint32_t mag_key(v_t a) { return (uint32_t)abs(a); }
+    static PD_INLINE acc_t acc(v_t a) { return a; }
+    static PD_INLINE acc_t add(acc_t a, acc_t b) { return a + b; }  // exact (reading C12)
+    static PD_INLINE bool acc_neg(acc_t a) { return a < 0; }
+};
+
+// ------------------------------------------------------------------- warp-scope sources
+// A source of node LLRs: a register stage (RegSrc) or a shared-memory stage (MemSrc, the
+// subtree root).  v(j): element lane + 32 j (N_v >= 64).  one(n): element lane (N_v <= 32,
+// lanes >= n unspecified).  pair(h, x, y): elements lane and lane + h (N_v = 2h <= 32).
+
+template <class P>
+struct RegSrc {
+    using V = typename P::v_t;
+    V* a;
+    PD_INLINE V v(int j) const { return a[j]; }
+    PD_INLINE V one(int) const { return a[0]; }
+    PD_INLINE void pair(int h, V& x, V& y) const {
+        x = a[0];
+        y = __shfl_down_sync(FULL, a[0], h);
+    }
+};
+
+template <class P, class T>
+struct MemSrc {
+    using V = typename P::v_t;
+    const T* p;
+    PD_INLINE V v(int j) const { return P::ld(p[lane_id() + 32 * j]); }
+    PD_INLINE V one(int n) const {
+        const unsigned l = lane_id();
+        return P::ld(p[l < (unsigned)n ? l : 0]);
+    }
+    PD_INLINE void pair(int h, V& x, V& y) const {
+        const unsigned l = lane_id() < (unsigned)h ? lane_id() : 0;
+        x = P::ld(p[l]);
+        y = P::ld(p[l + h]);
+    }
+};
+
+// ----------------------------------------------------------------- warp-scope operations
+
+// F<n>: child[i] = f(alpha[i], alpha[i + n/2]).
+template <class P, int n, class Src>
+PD_INLINE void wF(const Src& s, typename P::v_t* c) {
+    if constexpr (n >= 64) {
+#pragma unroll
+        for (int j = 0; j < n / 64; ++j) c[j] = P::f(s.v(j), s.v(j + n / 64));
+    } else {
+        typename P::v_t x, y;
+        s.pair(n / 2, x, y);
+        c[0] = P::f(x, y);
+    }
+}
+
+// G<n>: child[i] = g(alpha[i], alpha[i + n/2], beta_l[i]); beta_l from bw slots
+// s0.. (n >= 64) or from the left child's mask ml (n <= 32).
+template <class P, int n, int s0, class Src>
+PD_INLINE void wG(const Src& s, typename P::v_t* c, uint64_t bw, uint32_t ml) {
+    if constexpr (n >= 64) {
+#pragma unroll
+        for (int j = 0; j < n / 64; ++j)
+            c[j] = P::g(s.v(j), s.v(j + n / 64), (uint32_t)(bw >> (s0 + j)) & 1u);
+    } else {
+        typename P::v_t x, y;
+        s.pair(n / 2, x, y);
+        c[0] = P::g(x, y, (ml >> lane_id()) & 1u);
+    }
+}
+
+// G_0R<n>: G with beta_l = 0 (left child Rate-0).
+template <class P, int n, class Src>
+PD_INLINE void wG0R(const Src& s, typename P::v_t* c) {
+    if constexpr (n >= 64) {
+#pragma unroll
+        for (int j = 0; j < n / 64; ++j) c[j] = P::g0(s.v(j), s.v(j + n / 64));
+    } else {
+        typename P::v_t x, y;
+        s.pair(n / 2, x, y);
+        c[0] = P::g0(x, y);
+    }
+}
+
+// Rate-1 / Info<n> (eq:info P:444-449): beta = hard decisions.
+template <class P, int n, int s0, class Src>
+PD_INLINE void wR1(const Src& s, uint64_t& bw) {
+    static_assert(n >= 64, "");
+#pragma unroll
+    for (int j = 0; j < n / 32; ++j) bw |= (uint64_t)P::hd(s.v(j)) << (s0 + j);
+}
+template <class P, int n, class Src>
+PD_INLINE uint32_t wR1m(const Src& s) {
+    static_assert(n <= 32, "");
+    return __ballot_sync(FULL, P::hd(s.one(n))) & low_mask(n);
+}
+
+// Repetition<n>: all bits = [sum alpha < 0].  Sum in pairwise-halving order
+// x[i] += x[i + m/2], m = n, n/2, ..., 2 (reading C13): lane-local slot halving first, then
+// shuffles.  Returns the decision, uniform over the warp.
+template <class P, int n, class Src>
+PD_INLINE bool wRepDecide(const Src& s) {
+    using A = typename P::acc_t;
+    A t0;
+    int start;
+    if constexpr (n >= 64) {
+        A t[n / 32];
+#pragma unroll
+        for (int j = 0; j < n / 32; ++j) t[j] = P::acc(s.v(j));
+#pragma unroll
+        for (int m = n / 32; m > 1; m /= 2)
+#pragma unroll
+            for (int j = 0; j < m / 2; ++j) t[j] = P::add(t[j], t[j + m / 2]);
+        t0 = t[0];
+        start = 16;
+    } else {
+        t0 = P::acc(s.one(n));
+        start = n / 2;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o /= 2)
+        if (o <= start) t0 = P::add(t0, __shfl_down_sync(FULL, t0, o));
+    return __shfl_sync(FULL, (int)P::acc_neg(t0), 0) != 0;
+}
+template <class P, int n, int s0, class Src>
+PD_INLINE void wRep(const Src& s, uint64_t& bw) {
+    static_assert(n >= 64, "");
+    constexpr uint64_t span = (n / 32 == 64) ? ~0ull : (((1ull << (n / 32)) - 1ull) << s0);
+    if (wRepDecide<P, n>(s)) bw |= span;
+}
+template <class P, int n, class Src>
+PD_INLINE uint32_t wRepm(const Src& s) {
+    return wRepDecide<P, n>(s) ? low_mask(n) : 0u;
+}
+
+// SPC<n>: hard decisions; if their parity is odd flip the decision of the
+// least reliable bit, the lowest index among equal magnitudes (reading C10).
+template <class P, int n, class Src>
+PD_INLINE uint32_t wSPCm(const Src& s) {
+    static_assert(n <= 32, "");
+    const auto x = s.one(n);
+    const uint32_t hdm = __ballot_sync(FULL, P::hd(x)) & low_mask(n);
+    const uint32_t parity = __popc(hdm) & 1u;
+    const uint32_t key = lane_id() < (unsigned)n ? P::mag_key(x) : 0xffffffffu;
+    const uint32_t mn = __reduce_min_sync(FULL, key);
+    const uint32_t idx = __ffs(__ballot_sync(FULL, key == mn)) - 1;
+    return hdm ^ (parity << idx);
+}
+template <class P, int n, int s0, class Src>
+PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
+    static_assert(n >= 64, "");
+    uint64_t hb = 0;
+    uint32_t best = 0xffffffffu;
+    uint32_t bj = 0;
+#pragma unroll
+    for (int j = 0; j < n / 32; ++j) {
+        const auto x = s.v(j);
+        hb |= (uint64_t)P::hd(x) << j;
+        const uint32_t k = P::mag_key(x);
+        if (k < best) { best = k; bj = j; }
+    }
+    const uint32_t parity = __popc(__ballot_sync(FULL, __popcll(hb) & 1)) & 1u;
+    const uint32_t mn = __reduce_min_sync(FULL, best);
+    const uint32_t idx = __reduce_min_sync(FULL, best == mn ? bj * 32u + lane_id() : 0xffffffffu);
+    if (parity && lane_id() == (idx & 31u)) hb ^= 1ull << (idx >> 5);
+    bw |= hb << s0;
+}
+
+// Place the mask of a finished 32-bit node into bw slot s.
+template <int s>
+PD_INLINE void wDeposit(uint64_t& bw, uint32_t m) {
+    bw |= (uint64_t)((m >> lane_id()) & 1u) << s;
+}
+
+// Combine<n> / Combine_0R<n> on bw (n >= 64), eq:combine P:318-325:
+// left half of beta ^= right half; 0R: left half = right half (left was all zero).
+template <int n, int s0>
+PD_INLINE void wComb(uint64_t& bw) {
+    constexpr int h = n / 64;
+    constexpr uint64_t L = (((h == 64) ? ~0ull : ((1ull << h) - 1ull))) << s0;
+    bw ^= (bw >> h) & L;
+}
+template <int n, int s0>
+PD_INLINE void wComb0R(uint64_t& bw) {
+    constexpr int h = n / 64;
+    constexpr uint64_t L = (((h == 64) ? ~0ull : ((1ull << h) - 1ull))) << s0;
+    bw |= (bw >> h) & L;
+}
+
+// Write the beta of a finished warp subtree of size R >= 32 into the natural bit array:
+// word k (bits k*32 .. k*32+31 of the subtree) is the ballot of bw bit k.
+template <int R>
+PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
+    static_assert(R >= 32 && R <= 2048, "");
+    constexpr int NW = R / 32;
+    uint32_t keep[(NW + 31) / 32];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+        const uint32_t w = __ballot_sync(FULL, (uint32_t)(bw >> k) & 1u);
+        if (lane_id() == (unsigned)(k & 31)) keep[k >> 5] = w;
+    }
+#pragma unroll
+    for (int c = 0; c < (NW + 31) / 32; ++c)
+        if (lane_id() + 32 * c < (unsigned)NW) words[lane_id() + 32 * c] = keep[c];
+}
+
+// ------------------------------------------------------------------ CTA-scope operations
+// T threads; n > W >= 64; src/dst are shared-memory (or, for the f32 channel, global)
+// stages of the node; beta is the node's first word of the natural bit array.
+
+template <class P, int T, int n, class TS>
+PD_INLINE void cF(const TS* __restrict__ src, typename P::st_t* __restrict__ dst) {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n / 2; i += T) dst[i] = P::st(P::f(P::ld(src[i]), P::ld(src[i + n / 2])));
+}
+template <class P, int T, int n, class TS>
+PD_INLINE void cG(const TS* __restrict__ src, typename P::st_t* __restrict__ dst, const uint32_t* beta) {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n / 2; i += T)
+        dst[i] = P::st(P::g(P::ld(src[i]), P::ld(src[i + n / 2]), (beta[i >> 5] >> (i & 31)) & 1u));
+}
+template <class P, int T, int n, class TS>
+PD_INLINE void cG0R(const TS* __restrict__ src, typename P::st_t* __restrict__ dst) {
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n / 2; i += T) dst[i] = P::st(P::g0(P::ld(src[i]), P::ld(src[i + n / 2])));
+}
+template <class P, int T, int n, class TS>
+PD_INLINE void cR1(const TS* __restrict__ src, uint32_t* beta) {
+    for (int k = threadIdx.x >> 5; k < n / 32; k += T / 32) {
+        const uint32_t w = __ballot_sync(FULL, P::hd(P::ld(src[32 * k + lane_id()])));
+        if (lane_id() == 0) beta[k] = w;
+    }
+}
+// Repetition at CTA scope.  f32: pairwise-halving order (reading C13) run in
+// place on `scratch` (the free child stage of size n/2); int8: exact integer sum.
+template <class P, int T, int n, class TS>
+PD_INLINE void cRep(const TS* __restrict__ src, typename P::st_t* scratch, uint32_t* beta) {
+    __shared__ int red[T / 32];
+    __shared__ int decision;
+    const int warp = threadIdx.x >> 5;
+    if constexpr (P::kExactSum) {
+        typename P::acc_t s = 0;
+        for (int i = threadIdx.x; i < n; i += T) s = P::add(s, P::acc(P::ld(src[i])));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s = P::add(s, __shfl_xor_sync(FULL, s, o));
+        if (lane_id() == 0) red[warp] = (int)s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long tot = 0;
+            for (int w = 0; w < T / 32; ++w) tot += red[w];
+            decision = tot < 0;
+        }
+    } else {
+        for (int i = threadIdx.x; i < n / 2; i += T) scratch[i] = P::st(P::add(P::ld(src[i]), P::ld(src[i + n / 2])));
+        __syncthreads();
+        for (int m = n / 2; m > 32; m /= 2) {
+            for (int i = threadIdx.x; i < m / 2; i += T) scratch[i] = P::add(scratch[i], scratch[i + m / 2]);
+            __syncthreads();
+        }
+        if (warp == 0) {
+            typename P::acc_t t = scratch[lane_id()];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) t = P::add(t, __shfl_down_sync(FULL, t, o));
+            if (lane_id() == 0) decision = P::acc_neg(t);
+        }
+    }
+    __syncthreads();
+    const uint32_t w = decision ? FULL : 0u;
+    for (int k = threadIdx.x; k < n / 32; k += T) beta[k] = w;
+}
+
+// SPC at CTA scope: ballot hard decisions per word, parity of all, flip the
+// lowest-index least-magnitude bit when odd (reading C10); key = (|alpha| << 32) | index.
+template <class P, int T, int n, class TS>
+PD_INLINE void cSPC(const TS* __restrict__ src, uint32_t* beta) {
+    __shared__ unsigned long long red[T / 32];
+    __shared__ uint32_t par[T / 32];
+    const int warp = threadIdx.x >> 5;
+    unsigned long long best = ~0ull;
+    uint32_t p = 0;
+    for (int k = warp; k < n / 32; k += T / 32) {
+        const auto x = P::ld(src[32 * k + lane_id()]);
+        const uint32_t w = __ballot_sync(FULL, P::hd(x));
+        if (lane_id() == 0) beta[k] = w;
+        p ^= __popc(w) & 1u;
+        const unsigned long long key = ((unsigned long long)P::mag_key(x) << 32) | (uint32_t)(32 * k + lane_id());
+        best = key < best ? key : best;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(FULL, best, o);
+        best = other < best ? other : best;
+    }
+    if (lane_id() == 0) {
+        red[warp] = best;
+        par[warp] = p;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long b = ~0ull;
+        uint32_t q = 0;
+        for (int w = 0; w < T / 32; ++w) {
+            b = red[w] < b ? red[w] : b;
+            q ^= par[w];
+        }
+        if (q) {
+            const uint32_t idx = (uint32_t)b;
+            beta[idx >> 5] ^= 1u << (idx & 31);
+        }
+    }
+    __syncthreads();
+}
+
+template <int T, int n>
+PD_INLINE void cComb(uint32_t* beta) {
+    for (int k = threadIdx.x; k < n / 64; k += T) beta[k] ^= beta[k + n / 64];
+}
+template <int T, int n>
+PD_INLINE void cComb0R(uint32_t* beta) {
+    for (int k = threadIdx.x; k < n / 64; k += T) beta[k] = beta[k + n / 64];
+}
+
+// ----------------------------------------------------------------------- frame output
+// Systematic information bits x_hat[A] (reading C4/C5), packed LSB-first: word q holds
+// information bits 32q .. 32q+31 whose codeword positions are pos[32q ..].  One warp
+// produces words q0, q0 + qstep, ... (ballot per word) and stores them.
+template <int K>
+PD_INLINE void gather_info(const uint32_t* beta, const uint16_t* __restrict__ pos, uint32_t* __restrict__ out,
+                           int q0, int qstep) {
+    constexpr int NWK = (K + 31) / 32;
+    for (int q = q0; q < NWK; q += qstep) {
+        const int t = 32 * q + (int)lane_id();
+        uint32_t bit = 0;
+        if (t < K) {
+            const uint32_t p = __ldg(pos + t);
+            bit = (beta[p >> 5] >> (p & 31)) & 1u;
+        }
+        const uint32_t w = __ballot_sync(FULL, bit);
+        if (lane_id() == 0) out[q] = w;
+    }
+}
+
+// --------------------------------------------------------------- TMA bulk ingest helpers
+PD_INLINE uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+PD_INLINE void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+PD_INLINE void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+PD_INLINE void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// One elected thread: expect `bytes` on bar and start a bulk global->shared copy
+// (cp.async.bulk, completes on the mbarrier; bytes % 16 == 0, 16-B aligned addresses).
+PD_INLINE void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+PD_INLINE void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    const uint32_t a = smem_u32(bar);
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+}  // namespace pd

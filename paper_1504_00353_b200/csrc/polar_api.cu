@@ -1,0 +1,489 @@
+// polar_api.cu -- the C ABI of libpolar.so (include/polar.h).
+//
+// Hot path: polar_decode_f32 / polar_decode_i8 launch the decoder specialised at build time
+// for the handle's code (registry.hpp) on the caller's stream.  Everything else here is
+// non-hot: handle creation, GA construction, the systematic encoder, the BPSK-AWGN frame
+// generator, error counting and the host-buffer end-to-end path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/polar.h"
+#include "registry.hpp"
+#include "tree.hpp"
+
+namespace polar {
+void construct_ga(int N, int K, double design_ebn0_db, uint8_t* frozen);
+}
+
+using namespace polar;
+
+// ------------------------------------------------------------------------- errors
+
+static thread_local std::string g_last_error;
+
+static polar_status fail(polar_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return s;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(e_ == cudaErrorMemoryAllocation ? POLAR_ERR_OUT_OF_MEMORY : POLAR_ERR_CUDA, \
+                        "%s: %s", #expr, cudaGetErrorString(e_));                         \
+    } while (0)
+
+// ------------------------------------------------------------------------- handle
+
+struct polar_code {
+    uint32_t N = 0, K = 0;
+    std::vector<uint8_t> mask;
+    const RegistryEntry* entry = nullptr;
+    uint32_t n_ops = 0;
+    bool systematic_ok = false;  // information set closed under bit-superset (reading C4)
+    // device side (absent when no usable device at create time)
+    bool dev_ready = false;
+    int device = -1;
+    int n_sm = 0;
+    int occ_f32 = 0, occ_i8 = 0;  // resident CTAs per SM
+    uint16_t* d_pos = nullptr;    // K information positions, ascending
+    uint32_t* d_info_mask = nullptr;  // N/32 words (>= 1), bit set = information position
+    // host-buffer path (lazily allocated, guarded by mu)
+    std::mutex mu;
+    cudaStream_t streams[2] = {nullptr, nullptr};
+    void* d_stage_llr[2] = {nullptr, nullptr};
+    uint32_t* d_stage_out[2] = {nullptr, nullptr};
+    int64_t stage_frames = 0;
+    size_t stage_elem = 0;
+};
+
+static inline uint32_t words_of(uint32_t bits) { return (bits + 31) / 32; }
+
+extern "C" const char* polar_status_string(polar_status s) {
+    switch (s) {
+        case POLAR_OK: return "ok";
+        case POLAR_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case POLAR_ERR_UNSUPPORTED_CODE: return "unsupported code (no specialised decoder)";
+        case POLAR_ERR_CUDA: return "CUDA error";
+        case POLAR_ERR_OUT_OF_MEMORY: return "out of memory";
+    }
+    return "unknown status";
+}
+
+extern "C" const char* polar_last_error(void) { return g_last_error.c_str(); }
+
+static polar_status init_device(polar_code* h) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return POLAR_OK;  // host-only handle; decode calls will report POLAR_ERR_CUDA
+    }
+    CUDA_TRY(cudaGetDevice(&h->device));
+    CUDA_TRY(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
+    const RegistryEntry* e = h->entry;
+    const void* kf = *e->kern_f32;
+    const void* ki = *e->kern_i8;
+    CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*e->smem_f32));
+    CUDA_TRY(cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*e->smem_i8));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ_f32, kf, (int)e->threads, *e->smem_f32));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ_i8, ki, (int)e->threads, *e->smem_i8));
+    if (h->occ_f32 < 1 || h->occ_i8 < 1) return fail(POLAR_ERR_CUDA, "decoder kernel cannot be resident");
+    std::vector<uint16_t> pos;
+    std::vector<uint32_t> im(std::max<uint32_t>(1, h->N / 32), 0);
+    for (uint32_t i = 0; i < h->N; ++i)
+        if (!h->mask[i]) {
+            pos.push_back((uint16_t)i);
+            im[i / 32] |= 1u << (i % 32);
+        }
+    CUDA_TRY(cudaMalloc(&h->d_pos, pos.size() * sizeof(uint16_t)));
+    CUDA_TRY(cudaMemcpy(h->d_pos, pos.data(), pos.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&h->d_info_mask, im.size() * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemcpy(h->d_info_mask, im.data(), im.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    h->dev_ready = true;
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t* frozen_mask, polar_code** out) {
+    if (!out || !frozen_mask) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
+    *out = nullptr;
+    if (N < 2 || N > 32768 || (N & (N - 1))) return fail(POLAR_ERR_INVALID_ARGUMENT, "N=%u is not a power of two in [2, 32768]", N);
+    if (K < 1 || K > N) return fail(POLAR_ERR_INVALID_ARGUMENT, "K=%u not in [1, N]", K);
+    std::vector<uint8_t> m(frozen_mask, frozen_mask + N);
+    uint32_t nf = 0;
+    for (auto& b : m) {
+        b = b ? 1 : 0;
+        nf += b;
+    }
+    if (nf != N - K) return fail(POLAR_ERR_INVALID_ARGUMENT, "mask has %u frozen bits, expected N-K=%u", nf, N - K);
+    const uint64_t hsh = code_hash((int)N, (int)K, m.data());
+    const RegistryEntry* e = nullptr;
+    for (uint32_t i = 0; i < kRegistrySize; ++i)
+        if (kRegistry[i].hash == hsh && kRegistry[i].N == N && kRegistry[i].K == K &&
+            std::memcmp(kRegistry[i].mask, m.data(), N) == 0)
+            e = &kRegistry[i];
+    if (!e) return fail(POLAR_ERR_UNSUPPORTED_CODE, "no decoder was specialised for this (N=%u, K=%u) frozen set", N, K);
+    polar_code* h = new polar_code;
+    h->N = N;
+    h->K = K;
+    h->mask = std::move(m);
+    h->entry = e;
+    h->n_ops = (uint32_t)schedule(build_tree((int)N, h->mask.data())).size();
+    h->systematic_ok = superset_closed((int)N, h->mask.data());
+    polar_status s = init_device(h);
+    if (s != POLAR_OK) {
+        polar_code_destroy(h);
+        return s;
+    }
+    *out = h;
+    return POLAR_OK;
+}
+
+extern "C" void polar_code_destroy(polar_code* h) {
+    if (!h) return;
+    if (h->dev_ready) {
+        cudaFree(h->d_pos);
+        cudaFree(h->d_info_mask);
+        for (int i = 0; i < 2; ++i) {
+            if (h->d_stage_llr[i]) cudaFree(h->d_stage_llr[i]);
+            if (h->d_stage_out[i]) cudaFree(h->d_stage_out[i]);
+            if (h->streams[i]) cudaStreamDestroy(h->streams[i]);
+        }
+    }
+    delete h;
+}
+
+extern "C" polar_status polar_code_query(const polar_code* h, uint32_t* N, uint32_t* K, uint32_t* n_ops,
+                                         uint32_t* smem_bytes, uint32_t* warp_root) {
+    if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
+    if (N) *N = h->N;
+    if (K) *K = h->K;
+    if (n_ops) *n_ops = h->n_ops;
+    if (smem_bytes) *smem_bytes = *h->entry->smem_i8;
+    if (warp_root) *warp_root = h->entry->warp_root;
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_code_mask(const polar_code* h, uint8_t* mask_out) {
+    if (!h || !mask_out) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
+    std::memcpy(mask_out, h->mask.data(), h->N);
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_code_schedule(const polar_code* h, char* buf, uint32_t cap, uint32_t* needed) {
+    if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
+    const char* s = h->entry->schedule;
+    const uint32_t len = (uint32_t)std::strlen(s);
+    if (needed) *needed = len + 1;
+    if (buf && cap) {
+        const uint32_t n = std::min(len, cap - 1);
+        std::memcpy(buf, s, n);
+        buf[n] = 0;
+    }
+    return POLAR_OK;
+}
+
+extern "C" uint32_t polar_registry_size(void) { return kRegistrySize; }
+
+extern "C" polar_status polar_registry_entry(uint32_t i, uint32_t* N, uint32_t* K, uint8_t* mask_out) {
+    if (i >= kRegistrySize) return fail(POLAR_ERR_INVALID_ARGUMENT, "registry index %u out of range", i);
+    if (N) *N = kRegistry[i].N;
+    if (K) *K = kRegistry[i].K;
+    if (mask_out) std::memcpy(mask_out, kRegistry[i].mask, kRegistry[i].N);
+    return POLAR_OK;
+}
+
+// ------------------------------------------------------------------------- decode (hot)
+
+static polar_status launch_decode(const polar_code* h, bool i8, const void* llr, int64_t n, uint32_t* out,
+                                  cudaStream_t s) {
+    if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
+    if (n < 0) return fail(POLAR_ERR_INVALID_ARGUMENT, "n_frames < 0");
+    if (n == 0) return POLAR_OK;
+    if (!llr || !out) return fail(POLAR_ERR_INVALID_ARGUMENT, "null buffer");
+    if (((uintptr_t)llr & 15) != 0) return fail(POLAR_ERR_INVALID_ARGUMENT, "llr must be 16-byte aligned");
+    if (((uintptr_t)out & 3) != 0) return fail(POLAR_ERR_INVALID_ARGUMENT, "info_bits must be 4-byte aligned");
+    if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device was available when the handle was created");
+    const RegistryEntry* e = h->entry;
+    const void* kern = i8 ? *e->kern_i8 : *e->kern_f32;
+    const unsigned smem = i8 ? *e->smem_i8 : *e->smem_f32;
+    const int occ = i8 ? h->occ_i8 : h->occ_f32;
+    const int64_t need = (n + e->frames_per_cta - 1) / e->frames_per_cta;
+    const int64_t resident = (int64_t)occ * h->n_sm;
+    const unsigned grid = (unsigned)std::min(need, resident);
+    long long nn = (long long)n;
+    const uint16_t* pos = h->d_pos;
+    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&pos};
+    CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(e->threads), args, smem, s));
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_decode_f32(const polar_code* h, const float* llr, int64_t n, uint32_t* info,
+                                         polar_stream stream) {
+    return launch_decode(h, false, llr, n, info, (cudaStream_t)stream);
+}
+
+extern "C" polar_status polar_decode_i8(const polar_code* h, const int8_t* llr, int64_t n, uint32_t* info,
+                                        polar_stream stream) {
+    return launch_decode(h, true, llr, n, info, (cudaStream_t)stream);
+}
+
+// Host-buffer end-to-end path: chunks alternate over two streams so that the H2D copy of
+// one chunk, the decode of another and the D2H copy of a third overlap (P:1187-1189 idea).
+static polar_status decode_host(polar_code* h, bool i8, const void* host_llr, int64_t n, uint32_t* host_info) {
+    if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
+    if (n < 0) return fail(POLAR_ERR_INVALID_ARGUMENT, "n_frames < 0");
+    if (n == 0) return POLAR_OK;
+    if (!host_llr || !host_info) return fail(POLAR_ERR_INVALID_ARGUMENT, "null buffer");
+    if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device was available when the handle was created");
+    std::lock_guard<std::mutex> lock(h->mu);
+    const size_t elem = i8 ? 1 : 4;
+    const size_t frame_bytes = (size_t)h->N * elem;
+    const uint32_t wk = words_of(h->K);
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)((64u << 20) / frame_bytes)));
+    if (h->stage_frames < chunk || h->stage_elem < elem) {
+        for (int i = 0; i < 2; ++i) {
+            if (h->d_stage_llr[i]) cudaFree(h->d_stage_llr[i]);
+            if (h->d_stage_out[i]) cudaFree(h->d_stage_out[i]);
+            h->d_stage_llr[i] = nullptr;
+            h->d_stage_out[i] = nullptr;
+        }
+        h->stage_frames = 0;
+        for (int i = 0; i < 2; ++i) {
+            if (!h->streams[i]) CUDA_TRY(cudaStreamCreateWithFlags(&h->streams[i], cudaStreamNonBlocking));
+            CUDA_TRY(cudaMalloc(&h->d_stage_llr[i], chunk * (size_t)h->N * 4));
+            CUDA_TRY(cudaMalloc(&h->d_stage_out[i], chunk * (size_t)wk * 4));
+        }
+        h->stage_frames = chunk;
+        h->stage_elem = 4;
+    }
+    for (int64_t f0 = 0, c = 0; f0 < n; f0 += chunk, ++c) {
+        const int64_t m = std::min(chunk, n - f0);
+        const int b = (int)(c & 1);
+        cudaStream_t s = h->streams[b];
+        CUDA_TRY(cudaMemcpyAsync(h->d_stage_llr[b], (const char*)host_llr + f0 * frame_bytes, m * frame_bytes,
+                                 cudaMemcpyHostToDevice, s));
+        polar_status st = launch_decode(h, i8, h->d_stage_llr[b], m, h->d_stage_out[b], s);
+        if (st != POLAR_OK) return st;
+        CUDA_TRY(cudaMemcpyAsync(host_info + f0 * wk, h->d_stage_out[b], m * (size_t)wk * 4, cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(h->streams[0]));
+    CUDA_TRY(cudaStreamSynchronize(h->streams[1]));
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_decode_f32_host(polar_code* h, const float* host_llr, int64_t n, uint32_t* host_info) {
+    return decode_host(h, false, host_llr, n, host_info);
+}
+
+extern "C" polar_status polar_decode_i8_host(polar_code* h, const int8_t* host_llr, int64_t n, uint32_t* host_info) {
+    return decode_host(h, true, host_llr, n, host_info);
+}
+
+// ------------------------------------------------------------------------- construction
+
+extern "C" polar_status polar_construct_ga(uint32_t N, uint32_t K, double design_ebn0_db, uint8_t* mask_out) {
+    if (!mask_out) return fail(POLAR_ERR_INVALID_ARGUMENT, "null mask_out");
+    if (N < 2 || N > (1u << 24) || (N & (N - 1))) return fail(POLAR_ERR_INVALID_ARGUMENT, "N=%u is not a power of two", N);
+    if (K < 1 || K > N) return fail(POLAR_ERR_INVALID_ARGUMENT, "K=%u not in [1, N]", K);
+    if (!std::isfinite(design_ebn0_db)) return fail(POLAR_ERR_INVALID_ARGUMENT, "design Eb/N0 not finite");
+    construct_ga((int)N, (int)K, design_ebn0_db, mask_out);
+    return POLAR_OK;
+}
+
+// ------------------------------------------------------------------------- encoder / generator
+
+namespace {
+
+// Philox4x32-10 (Salmon et al., SC'11), counter (c0..c3), key (k0, k1).
+struct U4 {
+    uint32_t x, y, z, w;
+};
+__device__ __forceinline__ U4 philox(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return c;
+}
+
+// x <- x G_N on a packed codeword in shared memory (nw = N/32 words, or 1 word if N < 32):
+// x[j] ^= x[j | d] for every bit d of the index (G_N[i][j] = [j subset of i]).
+__device__ void transform_smem(uint32_t* x, int N, int nw) {
+    const uint32_t in_word[5] = {0x55555555u, 0x33333333u, 0x0F0F0F0Fu, 0x00FF00FFu, 0x0000FFFFu};
+    for (int b = 0; b < 5 && (1 << b) < N; ++b) {
+        const int d = 1 << b;
+        for (int k = threadIdx.x; k < nw; k += blockDim.x) x[k] ^= (x[k] >> d) & in_word[b];
+        __syncthreads();
+    }
+    for (int D = 1; D < nw; D <<= 1) {
+        for (int k = threadIdx.x; k < nw; k += blockDim.x)
+            if (!(k & D)) x[k] ^= x[k | D];
+        __syncthreads();
+    }
+}
+
+// Systematic codeword in smem from packed info bits (reading C4): v[A] = d, x = mask_A(vG) G.
+__device__ void systematic_smem(uint32_t* x, const uint32_t* info, const uint16_t* pos, const uint32_t* info_mask,
+                                int N, int K, int nw) {
+    for (int k = threadIdx.x; k < nw; k += blockDim.x) x[k] = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < K; t += blockDim.x)
+        if ((info[t >> 5] >> (t & 31)) & 1u) atomicOr(&x[pos[t] >> 5], 1u << (pos[t] & 31));
+    __syncthreads();
+    transform_smem(x, N, nw);
+    for (int k = threadIdx.x; k < nw; k += blockDim.x) x[k] &= info_mask[k];
+    __syncthreads();
+    transform_smem(x, N, nw);
+}
+
+__global__ void k_encode(const uint32_t* info, long long n, uint32_t* cw, const uint16_t* pos,
+                         const uint32_t* info_mask, int N, int K) {
+    extern __shared__ uint32_t x[];
+    const int nw = N >= 32 ? N / 32 : 1;
+    const int wk = (K + 31) / 32;
+    for (long long f = blockIdx.x; f < n; f += gridDim.x) {
+        systematic_smem(x, info + f * wk, pos, info_mask, N, K, nw);
+        for (int k = threadIdx.x; k < nw; k += blockDim.x) cw[f * nw + k] = x[k];
+        __syncthreads();
+    }
+}
+
+__global__ void k_gen(unsigned long long seed, unsigned long long first, long long n, float sigma, float llr_scale,
+                      float q_scale, float* llr_f32, int8_t* llr_i8, uint32_t* info_out, const uint16_t* pos,
+                      const uint32_t* info_mask, int N, int K) {
+    extern __shared__ uint32_t sm[];
+    const int nw = N >= 32 ? N / 32 : 1;
+    const int wk = (K + 31) / 32;
+    uint32_t* x = sm;
+    uint32_t* info = sm + nw;
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    for (long long f = blockIdx.x; f < n; f += gridDim.x) {
+        const unsigned long long g = first + (unsigned long long)f;
+        for (int q = threadIdx.x; q < wk; q += blockDim.x) {
+            uint32_t w = philox(U4{(uint32_t)g, (uint32_t)(g >> 32), (uint32_t)q, 0xB17u}, k0, k1).x;
+            if (q == wk - 1 && (K & 31)) w &= (1u << (K & 31)) - 1u;
+            info[q] = w;
+            if (info_out) info_out[f * wk + q] = w;
+        }
+        __syncthreads();
+        systematic_smem(x, info, pos, info_mask, N, K, nw);
+        // BPSK 0 -> +1, 1 -> -1; y = s + sigma n; LLR = 2 y / sigma^2 (readings C6/C7).
+        for (int q4 = threadIdx.x; q4 < (N + 3) / 4; q4 += blockDim.x) {
+            const U4 r = philox(U4{(uint32_t)g, (uint32_t)(g >> 32), (uint32_t)q4, 0xA3Cu}, k0, k1);
+            const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+            float nz[4];
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                const float u1 = ((float)u[2 * p] + 1.0f) * 2.3283064365386963e-10f;  // (0, 1]
+                const float u2 = (float)u[2 * p + 1] * 2.3283064365386963e-10f;
+                const float rad = sqrtf(-2.0f * logf(u1));
+                float sn, cs;
+                sincospif(2.0f * u2, &sn, &cs);
+                nz[2 * p] = rad * cs;
+                nz[2 * p + 1] = rad * sn;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int i = 4 * q4 + e;
+                if (i >= N) break;
+                const float s = ((x[i >> 5] >> (i & 31)) & 1u) ? -1.0f : 1.0f;
+                const float llr = llr_scale * (s + sigma * nz[e]);
+                if (llr_f32) llr_f32[f * N + i] = llr;
+                if (llr_i8) llr_i8[f * N + i] = (int8_t)fminf(fmaxf(rintf(q_scale * llr), -127.0f), 127.0f);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_count(const uint32_t* dec, const uint32_t* truth, long long n, int wk, unsigned long long* ctr) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long bits = 0, frames_bad = 0;
+    for (long long f = warp; f < n; f += nwarps) {
+        uint32_t e = 0;
+        for (int q = lane; q < wk; q += 32) {
+            const uint32_t d = dec[f * wk + q] ^ truth[f * wk + q];
+            e += __popc(d);
+        }
+        for (int o = 16; o; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        bits += e;
+        frames_bad += e != 0;
+    }
+    if (lane == 0) {
+        atomicAdd(&ctr[1], bits);
+        atomicAdd(&ctr[2], frames_bad);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ctr[0], (unsigned long long)n);
+}
+
+}  // namespace
+
+extern "C" polar_status polar_encode_systematic(const polar_code* h, const uint32_t* info, int64_t n, uint32_t* cw,
+                                                polar_stream stream) {
+    if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
+    if (n < 0) return fail(POLAR_ERR_INVALID_ARGUMENT, "n_frames < 0");
+    if (n == 0) return POLAR_OK;
+    if (!info || !cw) return fail(POLAR_ERR_INVALID_ARGUMENT, "null buffer");
+    if (!h->systematic_ok) return fail(POLAR_ERR_UNSUPPORTED_CODE, "information set not closed under bit-superset");
+    if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device");
+    const int nw = h->N >= 32 ? h->N / 32 : 1;
+    const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)h->n_sm * 16);
+    k_encode<<<grid, 256, nw * 4, (cudaStream_t)stream>>>(info, (long long)n, cw, h->d_pos, h->d_info_mask, (int)h->N,
+                                                          (int)h->K);
+    CUDA_TRY(cudaGetLastError());
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_gen_bpsk_awgn(const polar_code* h, uint64_t seed, uint64_t first_frame, int64_t n,
+                                            double ebn0_db, float q_scale, float* llr_f32, int8_t* llr_i8,
+                                            uint32_t* info, polar_stream stream) {
+    if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
+    if (n < 0) return fail(POLAR_ERR_INVALID_ARGUMENT, "n_frames < 0");
+    if (!std::isfinite(ebn0_db)) return fail(POLAR_ERR_INVALID_ARGUMENT, "Eb/N0 not finite");
+    if (n == 0) return POLAR_OK;
+    if (!h->systematic_ok) return fail(POLAR_ERR_UNSUPPORTED_CODE, "information set not closed under bit-superset");
+    if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device");
+    const double rate = (double)h->K / (double)h->N;
+    const double sigma2 = 1.0 / (2.0 * rate * std::pow(10.0, ebn0_db / 10.0));
+    const int nw = h->N >= 32 ? h->N / 32 : 1;
+    const int wk = (int)words_of(h->K);
+    const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)h->n_sm * 16);
+    k_gen<<<grid, 256, (nw + wk) * 4, (cudaStream_t)stream>>>(
+        (unsigned long long)seed, (unsigned long long)first_frame, (long long)n, (float)std::sqrt(sigma2),
+        (float)(2.0 / sigma2), q_scale, llr_f32, llr_i8, info, h->d_pos, h->d_info_mask, (int)h->N, (int)h->K);
+    CUDA_TRY(cudaGetLastError());
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_count_errors(const polar_code* h, const uint32_t* decoded, const uint32_t* truth,
+                                           int64_t n, int64_t* counters, polar_stream stream) {
+    if (!h || !decoded || !truth || !counters) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
+    if (n < 0) return fail(POLAR_ERR_INVALID_ARGUMENT, "n_frames < 0");
+    if (n == 0) return POLAR_OK;
+    if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device");
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 7) / 8, (int64_t)h->n_sm * 8);
+    k_count<<<grid, 256, 0, (cudaStream_t)stream>>>(decoded, truth, (long long)n, (int)words_of(h->K),
+                                                    (unsigned long long*)counters);
+    CUDA_TRY(cudaGetLastError());
+    return POLAR_OK;
+}

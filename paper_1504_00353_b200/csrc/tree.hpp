@@ -1,0 +1,126 @@
+// tree.hpp -- the Fast-SSC decoder tree of a polar code (host side, product code).
+//
+// Giard et al., arXiv:1504.00353: SC decoding is a depth-first traversal of the binary tree
+// of constituent codes; Fast-SSC stops the traversal at Rate-0 and
+// Rate-1 nodes, repetition nodes and single-parity-check nodes
+// (P:442-459).  The unrolled decoder is the list of operations met on that traversal
+// (Listing 1).  Node priority and the N_v = 2 rule follow reading C14 of
+// Rate-0 > Rate-1 > Rep > SPC > split.
+//
+// Used by the schedule emitter (codegen.cpp, build time) and by polar_code_create (to
+// validate the mask and report the op count).  Shares nothing with oracle/.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace polar {
+
+enum class Kind : int { Rate0 = 0, Rate1 = 1, Rep = 2, Spc = 3, Split = 4 };
+
+struct Node {
+    Kind kind;
+    int n;     // N_v, the node size
+    int off;   // index of the node's first bit in the codeword
+    int left;  // child indices into Tree::nodes (-1 for leaves)
+    int right;
+};
+
+struct Tree {
+    int N = 0;
+    std::vector<Node> nodes;  // nodes[0] is the root
+};
+
+// Classify the constituent code frozen[off .. off+n): counts of frozen bits decide.
+inline Kind classify(const uint8_t* frozen, int off, int n) {
+    int n_frozen = 0;
+    for (int i = off; i < off + n; ++i) n_frozen += frozen[i] != 0;
+    if (n_frozen == n) return Kind::Rate0;
+    if (n_frozen == 0) return Kind::Rate1;
+    if (n_frozen == n - 1 && frozen[off + n - 1] == 0) return Kind::Rep;
+    if (n_frozen == 1 && frozen[off] != 0) return Kind::Spc;
+    return Kind::Split;
+}
+
+inline int build_node(Tree& t, const uint8_t* frozen, int off, int n) {
+    int id = (int)t.nodes.size();
+    t.nodes.push_back(Node{classify(frozen, off, n), n, off, -1, -1});
+    if (t.nodes[id].kind == Kind::Split) {
+        int l = build_node(t, frozen, off, n / 2);
+        int r = build_node(t, frozen, off + n / 2, n / 2);
+        t.nodes[id].left = l;
+        t.nodes[id].right = r;
+    }
+    return id;
+}
+
+inline Tree build_tree(int N, const uint8_t* frozen) {
+    Tree t;
+    t.N = N;
+    build_node(t, frozen, 0, N);
+    return t;
+}
+
+// The unfused op list of the traversal, in Listing 1's vocabulary:
+// a split node whose left child is Rate-0 runs G_0R, its right subtree and Combine_0R;
+// any other split node runs F and its left subtree, then -- unless its right child is
+// Rate-0, where the right half of beta stays 0 (reading C16) -- G, its right subtree and
+// Combine.  Leaves emit Info (Rate-1), Repetition or SPC; Rate-0 leaves emit nothing.
+inline void schedule_rec(const Tree& t, int id, std::vector<std::string>& ops) {
+    const Node& v = t.nodes[id];
+    auto op = [&](const char* name) { ops.push_back(std::string(name) + "<" + std::to_string(v.n) + ">"); };
+    switch (v.kind) {
+        case Kind::Rate0: return;
+        case Kind::Rate1: op("Info"); return;
+        case Kind::Rep: op("Repetition"); return;
+        case Kind::Spc: op("SPC"); return;
+        case Kind::Split: break;
+    }
+    const Node& l = t.nodes[v.left];
+    const Node& r = t.nodes[v.right];
+    if (l.kind == Kind::Rate0) {
+        op("G_0R");
+        schedule_rec(t, v.right, ops);
+        op("Combine_0R");
+        return;
+    }
+    op("F");
+    schedule_rec(t, v.left, ops);
+    if (r.kind == Kind::Rate0) {
+        op("Combine_R0");
+        return;
+    }
+    op("G");
+    schedule_rec(t, v.right, ops);
+    op("Combine");
+}
+
+inline std::vector<std::string> schedule(const Tree& t) {
+    std::vector<std::string> ops;
+    schedule_rec(t, 0, ops);
+    return ops;
+}
+
+// Information set closed under bit-superset: i in A implies i | 2^b in A for every b.
+// Required by the two-pass systematic encoder (reading C4).
+inline bool superset_closed(int N, const uint8_t* frozen) {
+    for (int i = 0; i < N; ++i) {
+        if (frozen[i]) continue;
+        for (int b = 1; b < N; b <<= 1)
+            if (!(i & b) && frozen[i | b]) return false;
+    }
+    return true;
+}
+
+// FNV-1a over (N, K, mask bytes): the registry key of a specialised decoder.
+inline uint64_t code_hash(int N, int K, const uint8_t* frozen) {
+    uint64_t h = 1469598103934665603ull;
+    auto mix = [&](uint8_t b) { h ^= b; h *= 1099511628211ull; };
+    for (int s = 0; s < 32; s += 8) mix((uint8_t)(N >> s));
+    for (int s = 0; s < 32; s += 8) mix((uint8_t)(K >> s));
+    for (int i = 0; i < N; ++i) mix(frozen[i] ? 1 : 0);
+    return h;
+}
+
+}  // namespace polar

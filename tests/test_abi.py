@@ -1,0 +1,127 @@
+"""C-ABI library checks that need no GPU: the library loads, exports every symbol of
+include/polar.h, creates handles for its specialised codes, and its host-side logic (GA
+construction, Fast-SSC tree and op schedule) agrees with the oracle and the paper."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1504_00353_b200 as pb
+from seeded_inputs import random_mask
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "polar.h")
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def _declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(polar_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = pb.lib()
+    declared = _declared_symbols()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(L, name), name
+    assert sorted(pb.EXPORTS) == declared
+
+
+def test_status_strings():
+    L = pb.lib()
+    for s in range(5):
+        assert L.polar_status_string(s).decode()
+
+
+def _codes_spec():
+    """(name, N, K, how, arg) of every line of codes.txt / codes_random.txt."""
+    out = []
+    for fn in ("codes.txt", "codes_random.txt"):
+        for line in open(os.path.join(ROOT, "paper_1504_00353_b200", fn)):
+            line = line.split("#")[0].split()
+            if len(line) >= 5:
+                out.append((line[0], int(line[1]), int(line[2]), line[3], line[4]))
+    return out
+
+
+def test_registry_matches_spec_and_oracle_construction():
+    reg = pb.registry()
+    spec = _codes_spec()
+    assert len(reg) == len(spec)
+    for (N, K, m), (name, sN, sK, how, arg) in zip(reg, spec):
+        assert (N, K) == (sN, sK), name
+        assert int(m.sum()) == N - K
+        if how == "ga":
+            # product GA (csrc/construct.cpp) == oracle GA (oracle/polar_oracle.c), reading C1
+            np.testing.assert_array_equal(m, oracle.construct_ga(N, K, float(arg)), err_msg=name)
+        else:
+            np.testing.assert_array_equal(m, np.array([c == "1" for c in arg], np.uint8), err_msg=name)
+
+
+def test_construct_ga_matches_oracle_off_registry():
+    for N, K, e in [(64, 20, 1.0), (512, 300, 2.0), (4096, 1000, 0.5), (16384, 15000, 5.0)]:
+        np.testing.assert_array_equal(pb.construct_ga(N, K, e), oracle.construct_ga(N, K, e))
+
+
+def test_listing1_schedule_from_the_library():
+    """Listing 1 reproduced by the product's own schedule for the (8,5) code."""
+    lines = [l.strip() for l in open(os.path.join(GOLDEN, "listing1_8_5.txt")) if not l.startswith("#")]
+    mask = np.array([int(c) for c in lines[0]], np.uint8)
+    code = pb.PolarCode(8, 5, mask)
+    assert code.schedule() == [l for l in lines[1:] if l]
+    assert code.n_ops == 7
+
+
+def test_schedules_equal_oracle_traces():
+    for N, K, m in pb.registry():
+        code = pb.PolarCode(N, K, m)
+        assert code.schedule() == oracle.fastssc_trace(m), (N, K)
+
+
+@pytest.mark.parametrize("N,K,ops", [(1024, 512, 299), (2048, 1723, 371), (32768, 29492, 2607),
+                                     (32768, 27568, 3577)])
+def test_survey_op_counts(N, K, ops):
+    design = {1024: 2.5, 2048: 4.0, 29492: 4.5, 27568: 4.0}[N if N < 32768 else K]
+    assert pb.PolarCode.ga(N, K, design).n_ops == ops
+
+
+def test_create_validation():
+    m = pb.construct_ga(64, 32, 2.0)
+    with pytest.raises(pb.PolarError) as e:
+        pb.PolarCode(64, 33, m)  # popcount != N - K
+    assert e.value.status == pb.POLAR_ERR_INVALID_ARGUMENT
+    with pytest.raises(ValueError):
+        pb.PolarCode(64, 32, m[:32])
+    bad = np.zeros(48, np.uint8)
+    bad[:16] = 1
+    with pytest.raises(pb.PolarError) as e:
+        pb.PolarCode(48, 32, bad)  # N not a power of two
+    assert e.value.status == pb.POLAR_ERR_INVALID_ARGUMENT
+    with pytest.raises(pb.PolarError) as e:
+        pb.PolarCode(64, 32, random_mask(999, 64, 32))  # not specialised in this build
+    assert e.value.status == pb.POLAR_ERR_UNSUPPORTED_CODE
+
+
+def test_handle_roundtrip_and_query():
+    for N, K, m in pb.registry():
+        c = pb.PolarCode(N, K, m)
+        np.testing.assert_array_equal(c.mask(), m)
+        assert c.N == N and c.K == K and c.smem_bytes > 0
+        assert c.warp_root == (N if N <= 2048 else c.warp_root) and c.warp_root <= 2048
+        c.close()
+
+
+def test_no_cpu_fallback_without_gpu():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    c = pb.PolarCode(8, 5, np.array([1, 1, 0, 0, 1, 0, 0, 0], np.uint8))
+    llr = torch.zeros(1, 8)
+    out = torch.zeros(1, 1, dtype=torch.int32)
+    with pytest.raises(pb.PolarError) as e:
+        c.decode_f32(llr, out, stream=0)
+    assert e.value.status == pb.POLAR_ERR_CUDA

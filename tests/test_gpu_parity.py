@@ -1,0 +1,238 @@
+"""GPU parity: the sm_100a Fast-SSC kernels (through the C ABI) against the CPU oracle.
+
+Bar (north star): int8 bit-exact; f32 decision-exact -- the kernels use the oracle's op
+order with one IEEE add per g and no FMA, so f32 is compared bit-exactly as well.  Inputs
+are seeded synthetic frames (random information bits -> oracle systematic encoder -> BPSK
+-> AWGN, seeded_inputs) plus adversarial LLRs (ties, saturation, -128, huge magnitudes).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1504_00353_b200 as pb
+from seeded_inputs import bpsk_awgn_llr, draw, quantize_i8, random_llr_f32, random_llr_i8
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+THREADS = min(16, os.cpu_count() or 1)
+
+
+def _design():
+    """code name -> (N, K, mask, operating Eb/N0) for every specialised code."""
+    spec = {}
+    for fn in ("codes.txt", "codes_random.txt"):
+        for line in open(os.path.join(ROOT, "paper_1504_00353_b200", fn)):
+            f = line.split("#")[0].split()
+            if len(f) >= 5:
+                spec[(int(f[1]), int(f[2]), f[4] if f[3] == "mask" else None)] = (f[0], float(f[4]) if f[3] == "ga" else 2.0)
+    out = []
+    for N, K, m in pb.registry():
+        key = (N, K, "".join(str(int(b)) for b in m))
+        name, e = spec.get(key, spec.get((N, K, None), ("?", 2.0)))
+        out.append((name, N, K, m, e))
+    return out
+
+
+CODES = _design()
+
+
+def _n_frames(N):
+    return 400 if N <= 256 else 200 if N <= 2048 else 48 if N <= 8192 else 12
+
+
+def frames(mask, K, n, ebn0, seed, first=0):
+    N = mask.shape[0]
+    bits, noise = draw(seed, first, n, K, N)
+    x = oracle.encode_systematic(mask, bits)
+    llr = bpsk_awgn_llr(x, noise, ebn0, K)
+    return bits, llr, quantize_i8(llr)
+
+
+def expected(mask, llr):
+    x = oracle.fastssc_decode(mask, llr, threads=THREADS)
+    return oracle.pack_bits(oracle.info_bits(mask, x))
+
+
+def gpu_decode(code, llr):
+    t = torch.from_numpy(np.ascontiguousarray(llr)).cuda()
+    out = code.decode_i8(t) if llr.dtype == np.int8 else code.decode_f32(t)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().view(np.uint32)
+
+
+def assert_same(got, want, what):
+    bad = np.flatnonzero((got != want).any(axis=1))
+    assert bad.size == 0, f"{what}: {bad.size} of {len(want)} frames differ (first {bad[:8]})"
+
+
+@pytest.mark.parametrize("name,N,K,mask,ebn0", CODES, ids=[c[0] for c in CODES])
+@pytest.mark.parametrize("prof", ["f32", "i8"])
+def test_parity_awgn_frames(name, N, K, mask, ebn0, prof):
+    code = pb.PolarCode(N, K, mask)
+    n = _n_frames(N)
+    for k, e in enumerate((ebn0, ebn0 - 1.5)):  # operating point and a noisy point
+        _, llr, q = frames(mask, K, n, e, seed=1000 + k)
+        x = q if prof == "i8" else llr
+        assert_same(gpu_decode(code, x), expected(mask, x), f"{name} {prof} {e} dB")
+
+
+@pytest.mark.parametrize("name,N,K,mask,ebn0", CODES, ids=[c[0] for c in CODES])
+def test_parity_adversarial_llrs(name, N, K, mask, ebn0):
+    code = pb.PolarCode(N, K, mask)
+    n = max(8, _n_frames(N) // 4)
+    cases = {
+        "i8_uniform_full_range": random_llr_i8(7, (n, N), -128, 127),
+        "i8_small_ties": random_llr_i8(8, (n, N), -2, 2),
+        "i8_saturating": np.where(random_llr_i8(10, (n, N), 0, 1) > 0, 127, -128).astype(np.int8),
+        "i8_zero": np.zeros((2, N), np.int8),
+        "f32_gauss": random_llr_f32(11, (n, N), 3.0),
+        "f32_zero": np.zeros((2, N), np.float32),
+        "f32_huge": random_llr_f32(12, (n, N), 1e20),
+        "f32_ints_ties": random_llr_f32(13, (n, N), 1.0).round().astype(np.float32),
+    }
+    for what, x in cases.items():
+        assert_same(gpu_decode(code, x), expected(mask, x), f"{name} {what}")
+
+
+@pytest.mark.parametrize("name,N,K,mask,ebn0", [c for c in CODES if c[1] <= 4096], ids=[c[0] for c in CODES if c[1] <= 4096])
+def test_f32_equals_plain_sc(name, N, K, mask, ebn0):
+    """Pin 5: on f32 frames without exact-zero decisions, Fast-SSC == plain SC."""
+    code = pb.PolarCode(N, K, mask)
+    _, llr, _ = frames(mask, K, 64, ebn0 - 1.0, seed=77)
+    xs, _, zd = oracle.sc_decode(mask, llr, with_stats=True)
+    keep = zd == 0
+    want = oracle.pack_bits(oracle.info_bits(mask, xs))
+    assert_same(gpu_decode(code, llr)[keep], want[keep], name)
+
+
+def test_ragged_batches_and_grid_striding():
+    """Frame counts that are not multiples of the CTA's frames and exceed one resident wave."""
+    for (N, K, e) in [(64, 32, 2.0), (1024, 512, 2.5), (4096, 2048, 2.5)]:
+        mask = oracle.construct_ga(N, K, e)
+        code = pb.PolarCode(N, K, mask)
+        n = {64: 40013, 1024: 6007, 4096: 1201}[N]
+        x = random_llr_i8(21, (n, N), -40, 40)
+        assert_same(gpu_decode(code, x), expected(mask, x), f"({N},{K}) x{n}")
+
+
+def test_zero_frames_is_noop_and_bad_pointers_rejected():
+    mask = oracle.construct_ga(1024, 512, 2.5)
+    code = pb.PolarCode(1024, 512, mask)
+    out = torch.full((1, 16), 7, dtype=torch.int32, device="cuda")
+    code.decode_f32(torch.zeros(0, 1024, device="cuda"), out[:0])
+    torch.cuda.synchronize()
+    assert int(out[0, 0]) == 7
+    llr = torch.zeros(2 * 1024 + 1, device="cuda")
+    with pytest.raises(pb.PolarError) as e:
+        pb.lib()  # noqa
+        pb._check(pb.lib().polar_decode_f32(code._h, llr.data_ptr() + 4, 1, out.data_ptr(), None))
+    assert e.value.status == pb.POLAR_ERR_INVALID_ARGUMENT
+
+
+def test_batch1_and_full_size_32768():
+    """Batch-1 (config 3) and a throughput batch in the bench's launch configuration,
+    checked on every frame the oracle can afford."""
+    for K, e in [(29492, 4.5), (27568, 4.0)]:
+        mask = oracle.construct_ga(32768, K, e)
+        code = pb.PolarCode(32768, K, mask)
+        _, llr, q = frames(mask, K, 1, e, seed=5)
+        for x in (llr, q):
+            assert_same(gpu_decode(code, x), expected(mask, x), f"batch-1 {K} {x.dtype}")
+    code = pb.PolarCode(32768, 29492, oracle.construct_ga(32768, 29492, 4.5))
+    n = 4096
+    llr = torch.empty(n, 32768, dtype=torch.int8, device="cuda")
+    truth = torch.empty(n, code.info_words, dtype=torch.int32, device="cuda")
+    code.gen_bpsk_awgn(123, 0, n, 4.5, 4.0, llr_i8=llr, info=truth)
+    out = code.decode_i8(llr)
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(0).choice(n, 48, replace=False)
+    sample = llr[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert_same(out.cpu().numpy().view(np.uint32)[idx], expected(code.mask(), sample), "32768 sampled")
+
+
+def test_full_size_2048_1723_one_million_frames():
+    """Config 2 at full size (1M frames) in the bench's launch configuration: a sample of
+    frames against the oracle, and the frame-error rate against the truth bits."""
+    mask = oracle.construct_ga(2048, 1723, 4.0)
+    code = pb.PolarCode(2048, 1723, mask)
+    n = 1 << 20
+    llr = torch.empty(n, 2048, dtype=torch.int8, device="cuda")
+    truth = torch.empty(n, code.info_words, dtype=torch.int32, device="cuda")
+    code.gen_bpsk_awgn(1504000353, 0, n, 4.0, 4.0, llr_i8=llr, info=truth)
+    out = code.decode_i8(llr)
+    ctr = torch.zeros(3, dtype=torch.int64, device="cuda")
+    code.count_errors(out, truth, ctr)
+    torch.cuda.synchronize()
+    idx = np.random.default_rng(1).choice(n, 3000, replace=False)
+    idx.sort()
+    sample = llr[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert_same(out.cpu().numpy().view(np.uint32)[idx], expected(mask, sample), "1M sampled")
+    frames_, bit_err, frame_err = ctr.tolist()
+    assert frames_ == n
+    fer = frame_err / n
+    assert 0.005 < fer < 0.05, fer  # MC 1.9e-2 at 4.0 dB
+    assert bit_err >= frame_err
+
+
+def test_encoder_and_generator_against_oracle():
+    for N, K, e in [(8, 5, None), (1024, 512, 2.5), (2048, 1723, 4.0), (32768, 29492, 4.5)]:
+        mask = np.array([1, 1, 0, 0, 1, 0, 0, 0], np.uint8) if e is None else oracle.construct_ga(N, K, e)
+        code = pb.PolarCode(N, K, mask)
+        bits, _ = draw(3, 0, 16, K, N)
+        info = torch.from_numpy(oracle.pack_bits(bits).view(np.int32)).cuda()
+        cw = code.encode_systematic(info)
+        torch.cuda.synchronize()
+        want = oracle.pack_bits(oracle.encode_systematic(mask, bits))
+        np.testing.assert_array_equal(cw.cpu().numpy().view(np.uint32), want)
+        # generator: determinism across batching, the truth it reports is what it encoded
+        n = 64
+        l1 = torch.empty(n, N, device="cuda")
+        t1 = torch.empty(n, code.info_words, dtype=torch.int32, device="cuda")
+        code.gen_bpsk_awgn(9, 100, n, 3.0, 4.0, llr_f32=l1, info=t1)
+        l2 = torch.empty(n - 10, N, device="cuda")
+        code.gen_bpsk_awgn(9, 110, n - 10, 3.0, 4.0, llr_f32=l2)
+        q = torch.empty(n, N, dtype=torch.int8, device="cuda")
+        code.gen_bpsk_awgn(9, 100, n, 3.0, 4.0, llr_i8=q)
+        torch.cuda.synchronize()
+        assert torch.equal(l1[10:], l2)
+        np.testing.assert_array_equal(q.cpu().numpy(), quantize_i8(l1.cpu().numpy()))
+        tb = oracle.unpack_bits(t1.cpu().numpy().view(np.uint32), K)
+        x = oracle.encode_systematic(mask, tb).astype(np.float64)
+        s = 1.0 - 2.0 * x
+        s2 = 1.0 / (2 * (K / N) * 10 ** 0.3)
+        y = l1.cpu().numpy().astype(np.float64) * s2 / 2.0
+        noise = (y - s) / np.sqrt(s2)
+        assert abs(noise.mean()) < 0.05 and abs(noise.std() - 1.0) < 0.05
+
+
+def test_count_errors_matches_numpy():
+    code = pb.PolarCode(1024, 512, oracle.construct_ga(1024, 512, 2.5))
+    rng = np.random.default_rng(4)
+    a = rng.integers(0, 2**32, size=(1000, 16), dtype=np.uint64).astype(np.uint32)
+    b = a.copy()
+    flip = rng.random((1000, 16)) < 0.05
+    b[flip] ^= rng.integers(1, 2**32, size=int(flip.sum()), dtype=np.uint64).astype(np.uint32)
+    ctr = torch.zeros(3, dtype=torch.int64, device="cuda")
+    code.count_errors(torch.from_numpy(a.view(np.int32)).cuda(), torch.from_numpy(b.view(np.int32)).cuda(), ctr)
+    torch.cuda.synchronize()
+    bits = int(np.unpackbits((a ^ b).view(np.uint8)).sum())
+    fr = int(((a ^ b) != 0).any(axis=1).sum())
+    assert ctr.tolist() == [1000, bits, fr]
+
+
+def test_host_buffer_path_equals_device_path():
+    mask = oracle.construct_ga(2048, 1723, 4.0)
+    code = pb.PolarCode(2048, 1723, mask)
+    _, llr, q = frames(mask, 1723, 300, 3.5, seed=31)
+    for x in (llr, q):
+        host_out = np.zeros((300, code.info_words), np.uint32)
+        code.decode_host(np.ascontiguousarray(x), host_out)
+        np.testing.assert_array_equal(host_out, gpu_decode(code, x))
+        pinned = torch.from_numpy(x).pin_memory()
+        pout = torch.zeros(300, code.info_words, dtype=torch.int32).pin_memory()
+        code.decode_host(pinned, pout)
+        np.testing.assert_array_equal(pout.numpy().view(np.uint32), host_out)
