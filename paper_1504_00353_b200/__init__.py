@@ -24,7 +24,7 @@ POLAR_ERR_OUT_OF_MEMORY = 4
 # Every symbol include/polar.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "polar_status_string", "polar_last_error", "polar_code_create", "polar_code_destroy",
-    "polar_code_query", "polar_code_schedule", "polar_code_mask", "polar_decode_f32",
+    "polar_code_query", "polar_code_schedule", "polar_code_mask", "polar_code_set_variant", "polar_decode_f32",
     "polar_decode_i8", "polar_decode_f32_host", "polar_decode_i8_host", "polar_construct_ga",
     "polar_encode_systematic", "polar_gen_bpsk_awgn", "polar_count_errors",
     "polar_registry_size", "polar_registry_entry",
@@ -57,6 +57,7 @@ def lib() -> C.CDLL:
         "polar_code_query": (C.c_int, [vp, u32p, u32p, u32p, u32p, u32p]),
         "polar_code_schedule": (C.c_int, [vp, C.c_char_p, C.c_uint32, u32p]),
         "polar_code_mask": (C.c_int, [vp, vp]),
+        "polar_code_set_variant": (C.c_int, [vp, C.c_int]),
         "polar_decode_f32": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
         "polar_decode_i8": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
         "polar_decode_f32_host": (C.c_int, [vp, vp, C.c_int64, vp]),
@@ -149,6 +150,10 @@ class PolarCode:
             self.close()
         except Exception:
             pass
+
+    def set_variant(self, variant: str) -> None:
+        """'auto' | 'throughput' | 'latency' (both kernels decode identically)."""
+        _check(lib().polar_code_set_variant(self._h, {"auto": 0, "throughput": 1, "latency": 2}[variant]))
 
     def mask(self) -> np.ndarray:
         m = np.zeros(self.N, np.uint8)

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <fstream>
 #include <iostream>
+#include <algorithm>
 #include <map>
 #include <sstream>
 #include <string>
@@ -165,7 +166,7 @@ struct CtaEmitter {
         std::string fname = "sub" + std::to_string(n_subs++);
         emit_warp_sub(subs, t, id, fname);
         body << "        if (threadIdx.x < 32) " << fname << "<P>(" << src << ", beta);\n"
-             << "        __syncthreads();\n";
+             << "        group_sync<T>();\n";
     }
 
     void child(int id, const std::string& src) {
@@ -180,18 +181,19 @@ struct CtaEmitter {
         const int n = v.n;
         const std::string N_ = std::to_string(n);
         const std::string B = "(beta + " + std::to_string(v.off / 32) + ")";
+        const std::string CL = src == "chan" ? "true" : "false";  // int8 channel: clamp -128
         switch (v.kind) {
             case Kind::Rate0:
                 return;
             case Kind::Rate1:
-                body << "        cR1<P, T, " << N_ << ">(" << src << ", " << B << ");\n        __syncthreads();\n";
+                body << "        cR1<P, T, " << N_ << ">(" << src << ", " << B << ");\n        group_sync<T>();\n";
                 return;
             case Kind::Rep:
                 body << "        cRep<P, T, " << N_ << ">(" << src << ", " << stage(n / 2) << ", " << B
-                     << ");\n        __syncthreads();\n";
+                     << ");\n        group_sync<T>();\n";
                 return;
             case Kind::Spc:
-                body << "        cSPC<P, T, " << N_ << ">(" << src << ", " << B << ");\n        __syncthreads();\n";
+                body << "        cSPC<P, T, " << N_ << ">(" << src << ", " << B << ");\n        group_sync<T>();\n";
                 return;
             case Kind::Split:
                 break;
@@ -201,17 +203,17 @@ struct CtaEmitter {
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
         if (l.kind == Kind::Rate0) {
-            body << "        cG0R<P, T, " << N_ << ">(" << src << ", " << D << ");\n        __syncthreads();\n";
+            body << "        cG0R<P, T, " << N_ << ", " << CL << ">(" << src << ", " << D << ");\n        group_sync<T>();\n";
             child(v.right, D);
-            body << "        cComb0R<T, " << N_ << ">(" << B << ");\n        __syncthreads();\n";
+            body << "        cComb0R<T, " << N_ << ">(" << B << ");\n        group_sync<T>();\n";
             return;
         }
-        body << "        cF<P, T, " << N_ << ">(" << src << ", " << D << ");\n        __syncthreads();\n";
+        body << "        cF<P, T, " << N_ << ", " << CL << ">(" << src << ", " << D << ");\n        group_sync<T>();\n";
         child(v.left, D);
         if (r.kind == Kind::Rate0) return;
-        body << "        cG<P, T, " << N_ << ">(" << src << ", " << D << ", " << B << ");\n        __syncthreads();\n";
+        body << "        cG<P, T, " << N_ << ", " << CL << ", false>(" << src << ", " << D << ", " << B << ");\n        group_sync<T>();\n";
         child(v.right, D);
-        body << "        cComb<T, " << N_ << ">(" << B << ");\n        __syncthreads();\n";
+        body << "        cComb<T, " << N_ << ">(" << B << ");\n        group_sync<T>();\n";
     }
 };
 
@@ -225,67 +227,76 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                std::ostringstream& reg_entries) {
     Tree t = build_tree(sp.N, sp.mask.data());
     std::vector<std::string> ops = schedule(t);
-    const bool warp_mode = sp.N <= 2048;
+    const int W = std::min(sp.N, sp.W);
+    const bool cta_phase = sp.N > W;
+    const int t_lat = cta_phase ? sp.T : 32;
     std::ostringstream o;
     o << "// Generated by codegen.cpp for code " << sp.name << " (N=" << sp.N << ", K=" << sp.K
-      << ", " << ops.size() << " Fast-SSC ops). Do not edit.\n"
+      << ", " << ops.size() << " Fast-SSC ops, W=" << W << "). Do not edit.\n"
       << "#include \"kernels.cuh\"\n\nnamespace pd {\nnamespace code_" << sp.name << " {\n\n"
       << "struct Code {\n"
       << "    static constexpr int N = " << sp.N << ";\n"
-      << "    static constexpr int K = " << sp.K << ";\n";
-    if (warp_mode) {
-        o << "    static constexpr int WARPS = " << sp.warps << ";\n"
-          << "    static constexpr int MIN_BLOCKS = 1;\n";
+      << "    static constexpr int K = " << sp.K << ";\n"
+      << "    static constexpr int W = " << W << ";\n";
+    if (!cta_phase) {
+        o << "    static constexpr int STAGE_ELEMS = 0;\n";
         emit_warp_sub(o, t, 0, "decode_root");
-        o << "    template <class P>\n"
-          << "    static PD_INLINE void decode_warp(const typename P::in_t* chan, uint32_t* beta) {\n"
-          << "        decode_root<P>(chan, beta);\n    }\n";
+        o << "    template <class P, int T, class ChanT>\n"
+          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, uint32_t* beta) {\n"
+          << "        if (threadIdx.x < 32) decode_root<P>(chan, beta);\n    }\n";
     } else {
         std::ostringstream body, subs;
-        CtaEmitter ce{t, body, subs, sp.W, sp.T, sp.N, {}, 0};
+        CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, 0};
         int acc = 0;
-        for (int m = sp.N / 2; m >= sp.W; m /= 2) {
+        for (int m = sp.N / 2; m >= W; m /= 2) {
             ce.stage_off[m] = acc;
             acc += m;
         }
         ce.cta(0, "chan");
-        o << "    static constexpr int T = " << sp.T << ";\n"
-          << "    static constexpr int W = " << sp.W << ";\n"
-          << "    static constexpr int STAGE_ELEMS = " << acc << ";\n";
+        o << "    static constexpr int STAGE_ELEMS = " << acc << ";\n";
         o << subs.str();
-        o << "    template <class P, class ChanT>\n"
-          << "    static PD_INLINE void decode_cta(const ChanT* chan, typename P::st_t* stages, uint32_t* beta) {\n"
+        o << "    template <class P, int T, class ChanT>\n"
+          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, uint32_t* beta) {\n"
           << body.str() << "    }\n";
     }
     o << "};\n\n}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
-    const std::string kern = warp_mode ? "k_warp" : "k_cta";
-    const std::string lay = warp_mode ? "WarpLayout" : "CtaLayout";
     const std::string C = "pd::code_" + sp.name + "::Code";
-    o << "extern const void* const polar_kern_" << sp.name << "_f32 = (const void*)&pd::" << kern
-      << "<pd::PF32, " << C << ">;\n"
-      << "extern const void* const polar_kern_" << sp.name << "_i8 = (const void*)&pd::" << kern
-      << "<pd::PI8, " << C << ">;\n"
-      << "extern const unsigned polar_smem_" << sp.name << "_f32 = pd::" << lay << "<pd::PF32, " << C
-      << ">::SMEM;\n"
-      << "extern const unsigned polar_smem_" << sp.name << "_i8 = pd::" << lay << "<pd::PI8, " << C
-      << ">::SMEM;\n";
+    struct V {
+        const char* tag;
+        const char* prof;
+        int T;
+        bool chan_smem;
+    };
+    auto bytes = [&](const char* prof) { return sp.N * (std::string(prof) == "PF32" ? 4 : 1); };
+    std::vector<V> vars = {
+        {"tp_f32", "PF32", 32, 2 * bytes("PF32") <= 16384},
+        {"tp_i8", "PI8", 32, 2 * bytes("PI8") <= 16384},
+        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768},
+        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768},
+    };
+    for (auto& v : vars) {
+        const std::string targs = std::string("pd::") + v.prof + ", " + C + ", " + std::to_string(v.T) + ", " +
+                                  (v.chan_smem ? "true" : "false");
+        o << "extern const void* const polar_kern_" << sp.name << "_" << v.tag << " = (const void*)&pd::k_frame<"
+          << targs << ">;\n"
+          << "extern const unsigned polar_smem_" << sp.name << "_" << v.tag << " = pd::FrameLayout<" << targs
+          << ">::SMEM;\n";
+        reg_decl << "extern const void* const polar_kern_" << sp.name << "_" << v.tag << ";\n"
+                 << "extern const unsigned polar_smem_" << sp.name << "_" << v.tag << ";\n";
+    }
     std::ofstream(outdir + "/code_" + sp.name + ".cu") << o.str();
 
     std::string sched;
     for (auto& s : ops) sched += s + ";";
-    reg_decl << "extern const void* const polar_kern_" << sp.name << "_f32;\n"
-             << "extern const void* const polar_kern_" << sp.name << "_i8;\n"
-             << "extern const unsigned polar_smem_" << sp.name << "_f32;\n"
-             << "extern const unsigned polar_smem_" << sp.name << "_i8;\n"
-             << "static const uint8_t mask_" << sp.name << "[" << sp.N << "] = {";
+    reg_decl << "static const uint8_t mask_" << sp.name << "[" << sp.N << "] = {";
     for (int i = 0; i < sp.N; ++i) reg_decl << (i ? "," : "") << int(sp.mask[i]);
     reg_decl << "};\n";
     reg_entries << "    {\"" << sp.name << "\", " << sp.N << ", " << sp.K << ", mask_" << sp.name << ", "
-                << code_hash(sp.N, sp.K, sp.mask.data()) << "ull, " << ops.size() << ", "
-                << (warp_mode ? "MODE_WARP" : "MODE_CTA") << ", " << (warp_mode ? sp.N : sp.W) << ", "
-                << (warp_mode ? sp.warps * 32 : sp.T) << ", &polar_kern_" << sp.name << "_f32, &polar_kern_"
-                << sp.name << "_i8, &polar_smem_" << sp.name << "_f32, &polar_smem_" << sp.name << "_i8, "
-                << (warp_mode ? sp.warps : 1) << ", \"" << sched << "\"},\n";
+                << code_hash(sp.N, sp.K, sp.mask.data()) << "ull, " << ops.size() << ", " << W;
+    for (auto& v : vars)
+        reg_entries << ", {&polar_kern_" << sp.name << "_" << v.tag << ", &polar_smem_" << sp.name << "_" << v.tag
+                    << ", " << v.T << "}";
+    reg_entries << ", \"" << sched << "\"},\n";
 }
 
 }  // namespace

@@ -63,30 +63,109 @@ struct PF32 {
     static PD_INLINE bool acc_neg(acc_t a) { return a < 0.0f; }
 };
 
+// int8 profile: 8-bit storage (channel and shared-memory stages); registers hold the same
+// integers as f32, which is exact here (|values| <= 254 in any single g, sums < 2^24), so
+// f is one FMNMX with |.| modifiers plus the sign, and g one FADD plus the clamp.
 struct PI8 {
     using in_t = int8_t;
     using st_t = int8_t;
-    using v_t = int;
-    using acc_t = int;
-    static constexpr bool kExactSum = true;
+    using v_t = float;
+    using acc_t = float;
+    static constexpr bool kExactSum = true;  // integer sums below 2^24: any order is exact (C12)
     static constexpr bool kChanInSmem = true;
-    static PD_INLINE v_t ld(int8_t x) { return max((int)x, -127); }  // -128 -> -127 (C8)
-    static PD_INLINE int8_t st(v_t x) { return (int8_t)x; }
-    static PD_INLINE v_t f(v_t a, v_t b) {
-        const int m = min(abs(a), abs(b));
-        return (a ^ b) < 0 ? -m : m;
-    }
-    static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) {
-        const int s = beta ? b - a : b + a;
-        return min(max(s, -127), 127);  // saturating adder (max(-127) P:848)
-    }
-    static PD_INLINE v_t g0(v_t a, v_t b) { return min(max(b + a, -127), 127); }
-    static PD_INLINE bool hd(v_t a) { return a < 0; }
-    static PD_INLINE uint32_t mag_key(v_t a) { return (uint32_t)abs(a); }
+    // -128 -> -127 (C8); int -> float by the exponent trick (integer ALU + one FADD)
+    static PD_INLINE v_t ld(int8_t x) { return __int_as_float(0x4B400000 + max((int)x, -127)) - 12582912.0f; }
+    static PD_INLINE int8_t st(v_t x) { return (int8_t)__float2int_rn(x); }
+    static PD_INLINE v_t f(v_t a, v_t b) { return PF32::f(a, b); }
+    // saturating adder (max(-127) P:848)
+    static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) { return fminf(fmaxf(PF32::g(a, b, beta), -127.0f), 127.0f); }
+    static PD_INLINE v_t g0(v_t a, v_t b) { return fminf(fmaxf(__fadd_rn(b, a), -127.0f), 127.0f); }
+    static PD_INLINE bool hd(v_t a) { return a < 0.0f; }
+    static PD_INLINE uint32_t mag_key(v_t a) { return __float_as_uint(a) & 0x7fffffffu; }
     static PD_INLINE acc_t acc(v_t a) { return a; }
-    static PD_INLINE acc_t add(acc_t a, acc_t b) { return a + b; }  // exact (reading C12)
-    static PD_INLINE bool acc_neg(acc_t a) { return a < 0; }
+    static PD_INLINE acc_t add(acc_t a, acc_t b) { return __fadd_rn(a, b); }
+    static PD_INLINE bool acc_neg(acc_t a) { return a < 0.0f; }
 };
+
+// ------------------------------------------------------------- vector chunks (CTA scope)
+// CTA-scope ops move CE consecutive elements per thread: float4 (f32) or 4/8/16 packed int8.
+// int8 -> f32 by the exponent trick: bits 0x4B0000xx = 2^23 + xx with xx = byte ^ 0x80.
+PD_INLINE float i8_to_f(uint32_t biased_word, int k) {
+    return __uint_as_float(__byte_perm(biased_word, 0x4B000000u, 0x7440 + k)) - 8388736.0f;
+}
+// f32 holding an integer in [-128, 127] -> its two's-complement byte (low byte of the bits of
+// v + 1.5 * 2^23).
+PD_INLINE uint32_t f_to_i8bits(float v) { return __float_as_uint(__fadd_rn(v, 12582912.0f)); }
+
+template <class P, int CE>
+struct Chunk;
+
+template <int CE>
+struct Chunk<PF32, CE> {
+    static_assert(CE == 4, "");
+    float v[4];
+    PD_INLINE void load(const float* p) {
+        const float4 x = *reinterpret_cast<const float4*>(p);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    }
+    PD_INLINE void store(float* p) const { *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]); }
+};
+
+template <int CE>
+struct Chunk<PI8, CE> {
+    static_assert(CE == 4 || CE == 8 || CE == 16, "");
+    float v[CE];
+    PD_INLINE void unpack(const uint32_t* w, bool clamp) {
+#pragma unroll
+        for (int q = 0; q < CE / 4; ++q) {
+            const uint32_t b = w[q] ^ 0x80808080u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float x = i8_to_f(b, k);
+                v[4 * q + k] = clamp ? fmaxf(x, -127.0f) : x;
+            }
+        }
+    }
+    PD_INLINE void load(const int8_t* p, bool clamp = false) {
+        uint32_t w[CE / 4];
+        if constexpr (CE == 16) {
+            const uint4 x = *reinterpret_cast<const uint4*>(p);
+            w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+        } else if constexpr (CE == 8) {
+            const uint2 x = *reinterpret_cast<const uint2*>(p);
+            w[0] = x.x; w[1] = x.y;
+        } else {
+            w[0] = *reinterpret_cast<const uint32_t*>(p);
+        }
+        unpack(w, clamp);
+    }
+    PD_INLINE void store(int8_t* p) const {
+        uint32_t w[CE / 4];
+#pragma unroll
+        for (int q = 0; q < CE / 4; ++q) {
+            const uint32_t lo = __byte_perm(f_to_i8bits(v[4 * q]), f_to_i8bits(v[4 * q + 1]), 0x0040);
+            const uint32_t hi = __byte_perm(f_to_i8bits(v[4 * q + 2]), f_to_i8bits(v[4 * q + 3]), 0x0040);
+            w[q] = __byte_perm(lo, hi, 0x5410);
+        }
+        if constexpr (CE == 16) *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+        else if constexpr (CE == 8) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+        else *reinterpret_cast<uint32_t*>(p) = w[0];
+    }
+};
+
+// Elements per chunk for a CTA op over `half` outputs with T threads.
+template <class P, int half, int T>
+__host__ __device__ constexpr int chunk_elems() {
+    if constexpr (sizeof(typename P::st_t) == 4) return 4;
+    else return (half / T >= 16) ? 16 : (half / T >= 8) ? 8 : 4;
+}
+
+// Barrier of a T-thread frame group (a lone warp needs only __syncwarp).
+template <int T>
+PD_INLINE void group_sync() {
+    if constexpr (T == 32) __syncwarp();
+    else __syncthreads();
+}
 
 // ------------------------------------------------------------------- warp-scope sources
 // A source of node LLRs: a register stage (RegSrc) or a shared-memory stage (MemSrc, the
@@ -290,21 +369,47 @@ PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
 // T threads; n > W >= 64; src/dst are shared-memory (or, for the f32 channel, global)
 // stages of the node; beta is the node's first word of the natural bit array.
 
-template <class P, int T, int n, class TS>
+// CLAMP: the source is the channel (int8 -128 -> -127, reading C8); stages never need it.
+template <class P, int T, int n, bool CLAMP, class TS>
 PD_INLINE void cF(const TS* __restrict__ src, typename P::st_t* __restrict__ dst) {
-#pragma unroll 4
-    for (int i = threadIdx.x; i < n / 2; i += T) dst[i] = P::st(P::f(P::ld(src[i]), P::ld(src[i + n / 2])));
+    constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
+#pragma unroll 2
+    for (int i = CE * threadIdx.x; i < H; i += CE * T) {
+        Chunk<P, CE> a, b;
+        if constexpr (sizeof(typename P::st_t) == 1) {
+            a.load(src + i, CLAMP);
+            b.load(src + i + H, CLAMP);
+        } else {
+            a.load(src + i);
+            b.load(src + i + H);
+        }
+#pragma unroll
+        for (int k = 0; k < CE; ++k) a.v[k] = P::f(a.v[k], b.v[k]);
+        a.store(dst + i);
+    }
 }
-template <class P, int T, int n, class TS>
+template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, class TS>
 PD_INLINE void cG(const TS* __restrict__ src, typename P::st_t* __restrict__ dst, const uint32_t* beta) {
-#pragma unroll 4
-    for (int i = threadIdx.x; i < n / 2; i += T)
-        dst[i] = P::st(P::g(P::ld(src[i]), P::ld(src[i + n / 2]), (beta[i >> 5] >> (i & 31)) & 1u));
+    constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
+#pragma unroll 2
+    for (int i = CE * threadIdx.x; i < H; i += CE * T) {
+        Chunk<P, CE> a, b;
+        if constexpr (sizeof(typename P::st_t) == 1) {
+            a.load(src + i, CLAMP);
+            b.load(src + i + H, CLAMP);
+        } else {
+            a.load(src + i);
+            b.load(src + i + H);
+        }
+        const uint32_t bits = ZERO_LEFT ? 0u : (beta[i >> 5] >> (i & 31));
+#pragma unroll
+        for (int k = 0; k < CE; ++k) a.v[k] = P::g(a.v[k], b.v[k], (bits >> k) & 1u);
+        a.store(dst + i);
+    }
 }
-template <class P, int T, int n, class TS>
+template <class P, int T, int n, bool CLAMP, class TS>
 PD_INLINE void cG0R(const TS* __restrict__ src, typename P::st_t* __restrict__ dst) {
-#pragma unroll 4
-    for (int i = threadIdx.x; i < n / 2; i += T) dst[i] = P::st(P::g0(P::ld(src[i]), P::ld(src[i + n / 2])));
+    cG<P, T, n, CLAMP, true>(src, dst, nullptr);
 }
 template <class P, int T, int n, class TS>
 PD_INLINE void cR1(const TS* __restrict__ src, uint32_t* beta) {

@@ -59,7 +59,8 @@ struct polar_code {
     bool dev_ready = false;
     int device = -1;
     int n_sm = 0;
-    int occ_f32 = 0, occ_i8 = 0;  // resident CTAs per SM
+    int occ[4] = {0, 0, 0, 0};    // resident CTAs per SM: tp_f32, tp_i8, lat_f32, lat_i8
+    int variant = 0;              // 0 auto, 1 throughput, 2 latency (polar_code_set_variant)
     uint16_t* d_pos = nullptr;    // K information positions, ascending
     uint32_t* d_info_mask = nullptr;  // N/32 words (>= 1), bit set = information position
     // host-buffer path (lazily allocated, guarded by mu)
@@ -95,13 +96,13 @@ static polar_status init_device(polar_code* h) {
     CUDA_TRY(cudaGetDevice(&h->device));
     CUDA_TRY(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
     const RegistryEntry* e = h->entry;
-    const void* kf = *e->kern_f32;
-    const void* ki = *e->kern_i8;
-    CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*e->smem_f32));
-    CUDA_TRY(cudaFuncSetAttribute(ki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*e->smem_i8));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ_f32, kf, (int)e->threads, *e->smem_f32));
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ_i8, ki, (int)e->threads, *e->smem_i8));
-    if (h->occ_f32 < 1 || h->occ_i8 < 1) return fail(POLAR_ERR_CUDA, "decoder kernel cannot be resident");
+    const Variant* vs[4] = {&e->tp_f32, &e->tp_i8, &e->lat_f32, &e->lat_i8};
+    for (int i = 0; i < 4; ++i) {
+        const void* k = *vs[i]->kern;
+        CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*vs[i]->smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ[i], k, (int)vs[i]->threads, *vs[i]->smem));
+        if (h->occ[i] < 1) return fail(POLAR_ERR_CUDA, "decoder kernel variant %d cannot be resident", i);
+    }
     std::vector<uint16_t> pos;
     std::vector<uint32_t> im(std::max<uint32_t>(1, h->N / 32), 0);
     for (uint32_t i = 0; i < h->N; ++i)
@@ -172,8 +173,14 @@ extern "C" polar_status polar_code_query(const polar_code* h, uint32_t* N, uint3
     if (N) *N = h->N;
     if (K) *K = h->K;
     if (n_ops) *n_ops = h->n_ops;
-    if (smem_bytes) *smem_bytes = *h->entry->smem_i8;
+    if (smem_bytes) *smem_bytes = *h->entry->tp_i8.smem;
     if (warp_root) *warp_root = h->entry->warp_root;
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_code_set_variant(polar_code* h, int variant) {
+    if (!h || variant < 0 || variant > 2) return fail(POLAR_ERR_INVALID_ARGUMENT, "variant must be 0, 1 or 2");
+    h->variant = variant;
     return POLAR_OK;
 }
 
@@ -218,16 +225,19 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     if (((uintptr_t)out & 3) != 0) return fail(POLAR_ERR_INVALID_ARGUMENT, "info_bits must be 4-byte aligned");
     if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device was available when the handle was created");
     const RegistryEntry* e = h->entry;
-    const void* kern = i8 ? *e->kern_i8 : *e->kern_f32;
-    const unsigned smem = i8 ? *e->smem_i8 : *e->smem_f32;
-    const int occ = i8 ? h->occ_i8 : h->occ_f32;
-    const int64_t need = (n + e->frames_per_cta - 1) / e->frames_per_cta;
-    const int64_t resident = (int64_t)occ * h->n_sm;
-    const unsigned grid = (unsigned)std::min(need, resident);
+    // Latency variant (a CTA per frame) for batches that cannot fill the GPU with one frame
+    // per warp; otherwise the throughput variant (a warp per frame).
+    const bool lat = h->variant == 2 || (h->variant == 0 && n <= (int64_t)h->n_sm);
+    const int vi = (lat ? 2 : 0) + (i8 ? 1 : 0);
+    const Variant& v = vi == 0 ? e->tp_f32 : vi == 1 ? e->tp_i8 : vi == 2 ? e->lat_f32 : e->lat_i8;
+    const void* kern = *v.kern;
+    const unsigned smem = *v.smem;
+    const int64_t resident = (int64_t)h->occ[vi] * h->n_sm;
+    const unsigned grid = (unsigned)std::min<int64_t>(n, resident);
     long long nn = (long long)n;
     const uint16_t* pos = h->d_pos;
     void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&pos};
-    CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(e->threads), args, smem, s));
+    CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(v.threads), args, smem, s));
     return POLAR_OK;
 }
 

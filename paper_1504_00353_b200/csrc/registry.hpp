@@ -7,7 +7,13 @@
 
 namespace polar {
 
-enum : uint32_t { MODE_WARP = 0, MODE_CTA = 1 };
+// One compiled kernel: __global__ (const void* llr, long long n, uint32_t* out, const uint16_t* pos).
+// Held through pointers to per-code constants so the table is constant-initialised.
+struct Variant {
+    const void* const* kern;
+    const unsigned* smem;  // dynamic shared memory per CTA
+    uint32_t threads;      // threads per CTA = threads per frame
+};
 
 struct RegistryEntry {
     const char* name;
@@ -15,17 +21,10 @@ struct RegistryEntry {
     const uint8_t* mask;   // N bytes, 1 = frozen
     uint64_t hash;         // code_hash(N, K, mask)
     uint32_t n_ops;        // Listing-1 op count of the schedule
-    uint32_t mode;         // MODE_WARP: one warp per frame; MODE_CTA: one CTA per frame
     uint32_t warp_root;    // W: size of the subtrees decoded by one warp in registers
-    uint32_t threads;      // threads per CTA
-    // Addresses of the per-code constants (kept as pointers so the table is constant-
-    // initialised): kernel = __global__ (const void*, long long, uint32_t*, const uint16_t*).
-    const void* const* kern_f32;
-    const void* const* kern_i8;
-    const unsigned* smem_f32;  // dynamic shared memory per CTA
-    const unsigned* smem_i8;
-    uint32_t frames_per_cta;     // WARPS for MODE_WARP, 1 for MODE_CTA
-    const char* schedule;        // ';'-separated Listing-1 op list
+    Variant tp_f32, tp_i8;    // throughput: one warp per frame
+    Variant lat_f32, lat_i8;  // latency: one CTA of threads per frame
+    const char* schedule;     // ';'-separated Listing-1 op list
 };
 
 extern const RegistryEntry kRegistry[];

@@ -111,7 +111,7 @@ def test_handle_roundtrip_and_query():
         c = pb.PolarCode(N, K, m)
         np.testing.assert_array_equal(c.mask(), m)
         assert c.N == N and c.K == K and c.smem_bytes > 0
-        assert c.warp_root == (N if N <= 2048 else c.warp_root) and c.warp_root <= 2048
+        assert c.warp_root <= min(N, 2048) and c.warp_root & (c.warp_root - 1) == 0
         c.close()
 
 
