@@ -30,6 +30,28 @@ namespace pd {
 #define PD_INLINE __device__ __forceinline__
 constexpr unsigned FULL = 0xffffffffu;
 
+// min(|a|, |b|) carrying the sign sign(a) xor sign(b): f32 and f16x2 (sm_86+ PTX min.xorsign.abs)
+PD_INLINE float fminxs(float a, float b) {
+    float d;
+    asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+PD_INLINE uint32_t h2minxs(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.xorsign.abs.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+PD_INLINE uint32_t h2add(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+PD_INLINE uint32_t h2max(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
 PD_INLINE unsigned lane_id() { return threadIdx.x & 31u; }
 
 __host__ __device__ constexpr int slots(int n) { return n >= 32 ? n / 32 : 1; }
@@ -46,11 +68,10 @@ struct PF32 {
     static constexpr bool kChanInSmem = false;  // N=32768 f32 channel does not fit with the tree
     static PD_INLINE v_t ld(float x) { return x; }
     static PD_INLINE float st(v_t x) { return x; }
-    // eq:f: sgn(a) sgn(b) min(|a|, |b|)
-    static PD_INLINE v_t f(v_t a, v_t b) {
-        const float m = fminf(fabsf(a), fabsf(b));
-        return __uint_as_float(__float_as_uint(m) | ((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u));
-    }
+    // eq:f: sgn(a) sgn(b) min(|a|, |b|) -- one FMNMX.XORSIGN |a|, |b| (the sign
+    // is sign(a) xor sign(b); it differs from the comparison rule only on signed zeros,
+    // which no decision reads, reading C9)
+    static PD_INLINE v_t f(v_t a, v_t b) { return fminxs(a, b); }
     // eq:g: b + a if beta = 0 else b - a; beta flips the sign bit (P:817 idea)
     static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) {
         return __fadd_rn(b, __uint_as_float(__float_as_uint(a) ^ (beta << 31)));
@@ -77,9 +98,9 @@ struct PI8 {
     static PD_INLINE v_t ld(int8_t x) { return __int_as_float(0x4B400000 + max((int)x, -127)) - 12582912.0f; }
     static PD_INLINE int8_t st(v_t x) { return (int8_t)__float2int_rn(x); }
     static PD_INLINE v_t f(v_t a, v_t b) { return PF32::f(a, b); }
-    // saturating adder (max(-127) P:848)
-    static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) { return fminf(fmaxf(PF32::g(a, b, beta), -127.0f), 127.0f); }
-    static PD_INLINE v_t g0(v_t a, v_t b) { return fminf(fmaxf(__fadd_rn(b, a), -127.0f), 127.0f); }
+    // saturating adder (max(-127) P:848): clamp(x) = copysign(min(|x|, 127), x)
+    static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) { return fminxs(PF32::g(a, b, beta), 127.0f); }
+    static PD_INLINE v_t g0(v_t a, v_t b) { return fminxs(__fadd_rn(b, a), 127.0f); }
     static PD_INLINE bool hd(v_t a) { return a < 0.0f; }
     static PD_INLINE uint32_t mag_key(v_t a) { return __float_as_uint(a) & 0x7fffffffu; }
     static PD_INLINE acc_t acc(v_t a) { return a; }
@@ -89,13 +110,6 @@ struct PI8 {
 
 // ------------------------------------------------------------- vector chunks (CTA scope)
 // CTA-scope ops move CE consecutive elements per thread: float4 (f32) or 4/8/16 packed int8.
-// int8 -> f32 by the exponent trick: bits 0x4B0000xx = 2^23 + xx with xx = byte ^ 0x80.
-PD_INLINE float i8_to_f(uint32_t biased_word, int k) {
-    return __uint_as_float(__byte_perm(biased_word, 0x4B000000u, 0x7440 + k)) - 8388736.0f;
-}
-// f32 holding an integer in [-128, 127] -> its two's-complement byte (low byte of the bits of
-// v + 1.5 * 2^23).
-PD_INLINE uint32_t f_to_i8bits(float v) { return __float_as_uint(__fadd_rn(v, 12582912.0f)); }
 
 template <class P, int CE>
 struct Chunk;
@@ -111,18 +125,22 @@ struct Chunk<PF32, CE> {
     PD_INLINE void store(float* p) const { *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]); }
 };
 
+// int8 stages are processed as integer-valued f16x2 (exact: |values| <= 254 before the clamp).
+// unpack: t = w ^ 0x80808080 (bias 128), halves 0x64tt = 1024 + t, minus 1152 -> the value.
+// pack: + 1152 -> 0x64tt, gather the low bytes, remove the bias.
 template <int CE>
 struct Chunk<PI8, CE> {
     static_assert(CE == 4 || CE == 8 || CE == 16, "");
-    float v[CE];
+    uint32_t h[CE / 2];
     PD_INLINE void unpack(const uint32_t* w, bool clamp) {
 #pragma unroll
         for (int q = 0; q < CE / 4; ++q) {
-            const uint32_t b = w[q] ^ 0x80808080u;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float x = i8_to_f(b, k);
-                v[4 * q + k] = clamp ? fmaxf(x, -127.0f) : x;
+            const uint32_t t = w[q] ^ 0x80808080u;
+            h[2 * q] = h2add(__byte_perm(t, 0x64646464u, 0x4140), 0xE480E480u);
+            h[2 * q + 1] = h2add(__byte_perm(t, 0x64646464u, 0x4342), 0xE480E480u);
+            if (clamp) {  // channel input: -128 -> -127 (reading C8)
+                h[2 * q] = h2max(h[2 * q], 0xD7F0D7F0u);
+                h[2 * q + 1] = h2max(h[2 * q + 1], 0xD7F0D7F0u);
             }
         }
     }
@@ -142,16 +160,54 @@ struct Chunk<PI8, CE> {
     PD_INLINE void store(int8_t* p) const {
         uint32_t w[CE / 4];
 #pragma unroll
-        for (int q = 0; q < CE / 4; ++q) {
-            const uint32_t lo = __byte_perm(f_to_i8bits(v[4 * q]), f_to_i8bits(v[4 * q + 1]), 0x0040);
-            const uint32_t hi = __byte_perm(f_to_i8bits(v[4 * q + 2]), f_to_i8bits(v[4 * q + 3]), 0x0040);
-            w[q] = __byte_perm(lo, hi, 0x5410);
-        }
+        for (int q = 0; q < CE / 4; ++q)
+            w[q] = __byte_perm(h2add(h[2 * q], 0x64806480u), h2add(h[2 * q + 1], 0x64806480u), 0x6420) ^ 0x80808080u;
         if constexpr (CE == 16) *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
         else if constexpr (CE == 8) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
         else *reinterpret_cast<uint32_t*>(p) = w[0];
     }
+    // F: h = f(h, b)
+    PD_INLINE void f(const Chunk& b) {
+#pragma unroll
+        for (int q = 0; q < CE / 2; ++q) h[q] = h2minxs(h[q], b.h[q]);
+    }
+    // G: h = sat(b + (beta ? -h : h)); bit k of `bits` is beta of element k; the saturation
+    // is min.xorsign.abs against 127.
+    PD_INLINE void g(const Chunk& b, uint32_t bits) {
+#pragma unroll
+        for (int q = 0; q < CE / 2; ++q) {
+            const uint32_t lo = (bits << (15 - 2 * q)) & 0x8000u;
+            const uint32_t hi = (bits << (30 - 2 * q)) & 0x80000000u;
+            h[q] = h2minxs(h2add(b.h[q], h[q] ^ (lo | hi)), 0x57F057F0u);
+        }
+    }
+    PD_INLINE void g0(const Chunk& b) {
+#pragma unroll
+        for (int q = 0; q < CE / 2; ++q) h[q] = h2minxs(h2add(b.h[q], h[q]), 0x57F057F0u);
+    }
 };
+
+template <int CE>
+PD_INLINE void chunk_f(Chunk<PF32, CE>& a, const Chunk<PF32, CE>& b) {
+#pragma unroll
+    for (int k = 0; k < CE; ++k) a.v[k] = PF32::f(a.v[k], b.v[k]);
+}
+template <int CE>
+PD_INLINE void chunk_g(Chunk<PF32, CE>& a, const Chunk<PF32, CE>& b, uint32_t bits) {
+#pragma unroll
+    for (int k = 0; k < CE; ++k) a.v[k] = PF32::g(a.v[k], b.v[k], (bits >> k) & 1u);
+}
+template <int CE>
+PD_INLINE void chunk_g0(Chunk<PF32, CE>& a, const Chunk<PF32, CE>& b) {
+#pragma unroll
+    for (int k = 0; k < CE; ++k) a.v[k] = PF32::g0(a.v[k], b.v[k]);
+}
+template <int CE>
+PD_INLINE void chunk_f(Chunk<PI8, CE>& a, const Chunk<PI8, CE>& b) { a.f(b); }
+template <int CE>
+PD_INLINE void chunk_g(Chunk<PI8, CE>& a, const Chunk<PI8, CE>& b, uint32_t bits) { a.g(b, bits); }
+template <int CE>
+PD_INLINE void chunk_g0(Chunk<PI8, CE>& a, const Chunk<PI8, CE>& b) { a.g0(b); }
 
 // Elements per chunk for a CTA op over `half` outputs with T threads.
 template <class P, int half, int T>
@@ -383,8 +439,7 @@ PD_INLINE void cF(const TS* __restrict__ src, typename P::st_t* __restrict__ dst
             a.load(src + i);
             b.load(src + i + H);
         }
-#pragma unroll
-        for (int k = 0; k < CE; ++k) a.v[k] = P::f(a.v[k], b.v[k]);
+        chunk_f(a, b);
         a.store(dst + i);
     }
 }
@@ -401,9 +456,8 @@ PD_INLINE void cG(const TS* __restrict__ src, typename P::st_t* __restrict__ dst
             a.load(src + i);
             b.load(src + i + H);
         }
-        const uint32_t bits = ZERO_LEFT ? 0u : (beta[i >> 5] >> (i & 31));
-#pragma unroll
-        for (int k = 0; k < CE; ++k) a.v[k] = P::g(a.v[k], b.v[k], (bits >> k) & 1u);
+        if constexpr (ZERO_LEFT) chunk_g0(a, b);
+        else chunk_g(a, b, beta[i >> 5] >> (i & 31));
         a.store(dst + i);
     }
 }
@@ -508,23 +562,45 @@ PD_INLINE void cComb0R(uint32_t* beta) {
 }
 
 // ----------------------------------------------------------------------- frame output
-// Systematic information bits x_hat[A] (reading C4/C5), packed LSB-first: word q holds
-// information bits 32q .. 32q+31 whose codeword positions are pos[32q ..].  One warp
-// produces words q0, q0 + qstep, ... (ballot per word) and stores them.
-template <int K>
-PD_INLINE void gather_info(const uint32_t* beta, const uint16_t* __restrict__ pos, uint32_t* __restrict__ out,
-                           int q0, int qstep) {
-    constexpr int NWK = (K + 31) / 32;
-    for (int q = q0; q < NWK; q += qstep) {
-        const int t = 32 * q + (int)lane_id();
-        uint32_t bit = 0;
-        if (t < K) {
-            const uint32_t p = __ldg(pos + t);
-            bit = (beta[p >> 5] >> (p & 31)) & 1u;
-        }
-        const uint32_t w = __ballot_sync(FULL, bit);
-        if (lane_id() == 0) out[q] = w;
+// Systematic information bits x_hat[A] (reading C4/C5), packed LSB-first, A ascending.
+// x_hat[A] is the codeword with the frozen positions squeezed out: for every codeword word k
+// the information bits are pext(beta[k], imask[k]) and land at bit offset prefix[k] of the
+// output (tab = {imask[0..NB), prefix[0..NB)}, NB = max(1, N/32), built at create time).
+// The group's threads take codeword words k = tid, tid + T, ... and OR their runs into the
+// shared staging words `stg` (ceil(K/32) words), which are then stored coalesced.
+PD_INLINE uint32_t pext32(uint32_t x, uint32_t m) {
+    if (m == 0xffffffffu) return x;
+    uint32_t r = 0, at = 0;
+    while (m) {
+        const uint32_t s = __ffs(m) - 1;          // start of the lowest run of ones
+        const uint32_t t = ~(m >> s);             // zeros where the run continues
+        const uint32_t len = t ? __ffs(t) - 1 : 32 - s;
+        const uint32_t lm = len >= 32 ? 0xffffffffu : ((1u << len) - 1u);
+        r |= ((x >> s) & lm) << at;
+        at += len;
+        m &= ~(lm << s);
     }
+    return r;
+}
+
+template <int N, int K, int T>
+PD_INLINE void gather_info(const uint32_t* beta, const uint32_t* __restrict__ tab, uint32_t* stg,
+                           uint32_t* __restrict__ out) {
+    constexpr int NB = N >= 32 ? N / 32 : 1;
+    constexpr int NWK = (K + 31) / 32;
+    for (int q = threadIdx.x; q < NWK; q += T) stg[q] = 0;
+    group_sync<T>();
+    for (int k = threadIdx.x; k < NB; k += T) {
+        const uint32_t m = __ldg(tab + k);
+        if (!m) continue;
+        const uint32_t p = __ldg(tab + NB + k);
+        const uint32_t r = pext32(beta[k], m);
+        const uint32_t sh = p & 31;
+        atomicOr(stg + (p >> 5), r << sh);
+        if (sh && sh + __popc(m) > 32) atomicOr(stg + (p >> 5) + 1, r >> (32 - sh));
+    }
+    group_sync<T>();
+    for (int q = threadIdx.x; q < NWK; q += T) out[q] = stg[q];
 }
 
 // --------------------------------------------------------------- TMA bulk ingest helpers

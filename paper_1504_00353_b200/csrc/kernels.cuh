@@ -37,13 +37,16 @@ struct FrameLayout {
     static constexpr int BUF = align16(FRAME_BYTES);
     static constexpr int STAGES = align16(C::STAGE_ELEMS * (int)sizeof(st_t));
     static constexpr int BETA = align16((C::N >= 32 ? C::N / 32 : 1) * 4);
-    static constexpr int SMEM = NBUF * BUF + STAGES + BETA + 16;
+    // output staging words: the stage area is free after the decode when it is large enough
+    static constexpr int OUTW = align16((C::K + 31) / 32 * 4);
+    static constexpr int STG = STAGES >= OUTW ? 0 : OUTW;
+    static constexpr int SMEM = NBUF * BUF + STAGES + BETA + STG + 16;
 };
 
 template <class P, class C, int T, bool CHAN_SMEM>
 __global__ void __launch_bounds__(T)
     k_frame(const void* __restrict__ llr_, long long n_frames, uint32_t* __restrict__ out,
-            const uint16_t* __restrict__ pos) {
+            const uint32_t* __restrict__ gtab) {
     using L = FrameLayout<P, C, T, CHAN_SMEM>;
     using in_t = typename P::in_t;
     using st_t = typename P::st_t;
@@ -56,7 +59,8 @@ __global__ void __launch_bounds__(T)
     in_t* const buf1 = (in_t*)(smem + (DBL ? L::BUF : 0));
     st_t* const stages = (st_t*)(smem + L::NBUF * L::BUF);
     uint32_t* const beta = (uint32_t*)(smem + L::NBUF * L::BUF + L::STAGES);
-    uint64_t* const bar = (uint64_t*)(smem + L::NBUF * L::BUF + L::STAGES + L::BETA);
+    uint32_t* const stg = (uint32_t*)(L::STG ? smem + L::NBUF * L::BUF + L::STAGES + L::BETA : (unsigned char*)stages);
+    uint64_t* const bar = (uint64_t*)(smem + L::NBUF * L::BUF + L::STAGES + L::BETA + L::STG);
     const in_t* llr = (const in_t*)llr_;
 
     long long f = blockIdx.x;
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(T)
         }
         C::template decode<P, T>(chan, stages, beta);
         group_sync<T>();
-        gather_info<C::K>(beta, pos, out + f * NWK, threadIdx.x >> 5, T / 32);
+        gather_info<N, C::K, T>(beta, gtab, stg, out + f * NWK);
         group_sync<T>();
         if constexpr (TMA && !DBL) {
             // single buffer: the next frame's copy starts once every thread is done with this one

@@ -61,7 +61,8 @@ struct polar_code {
     int n_sm = 0;
     int occ[4] = {0, 0, 0, 0};    // resident CTAs per SM: tp_f32, tp_i8, lat_f32, lat_i8
     int variant = 0;              // 0 auto, 1 throughput, 2 latency (polar_code_set_variant)
-    uint16_t* d_pos = nullptr;    // K information positions, ascending
+    uint16_t* d_pos = nullptr;    // K information positions, ascending (encoder / generator)
+    uint32_t* d_gtab = nullptr;   // gather table: info mask words, then info-bit prefix per word
     uint32_t* d_info_mask = nullptr;  // N/32 words (>= 1), bit set = information position
     // host-buffer path (lazily allocated, guarded by mu)
     std::mutex mu;
@@ -112,6 +113,14 @@ static polar_status init_device(polar_code* h) {
         }
     CUDA_TRY(cudaMalloc(&h->d_pos, pos.size() * sizeof(uint16_t)));
     CUDA_TRY(cudaMemcpy(h->d_pos, pos.data(), pos.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    std::vector<uint32_t> gt(im);
+    uint32_t acc = 0;
+    for (uint32_t w : im) {
+        gt.push_back(acc);
+        acc += (uint32_t)__builtin_popcount(w);
+    }
+    CUDA_TRY(cudaMalloc(&h->d_gtab, gt.size() * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemcpy(h->d_gtab, gt.data(), gt.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMalloc(&h->d_info_mask, im.size() * sizeof(uint32_t)));
     CUDA_TRY(cudaMemcpy(h->d_info_mask, im.data(), im.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     h->dev_ready = true;
@@ -158,6 +167,7 @@ extern "C" void polar_code_destroy(polar_code* h) {
     if (h->dev_ready) {
         cudaFree(h->d_pos);
         cudaFree(h->d_info_mask);
+        cudaFree(h->d_gtab);
         for (int i = 0; i < 2; ++i) {
             if (h->d_stage_llr[i]) cudaFree(h->d_stage_llr[i]);
             if (h->d_stage_out[i]) cudaFree(h->d_stage_out[i]);
@@ -235,8 +245,8 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     const int64_t resident = (int64_t)h->occ[vi] * h->n_sm;
     const unsigned grid = (unsigned)std::min<int64_t>(n, resident);
     long long nn = (long long)n;
-    const uint16_t* pos = h->d_pos;
-    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&pos};
+    const uint32_t* gtab = h->d_gtab;
+    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab};
     CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(v.threads), args, smem, s));
     return POLAR_OK;
 }

@@ -7,7 +7,7 @@
 
 namespace polar {
 
-// One compiled kernel: __global__ (const void* llr, long long n, uint32_t* out, const uint16_t* pos).
+// One compiled kernel: __global__ (const void* llr, long long n, uint32_t* out, const uint32_t* gtab).
 // Held through pointers to per-code constants so the table is constant-initialised.
 struct Variant {
     const void* const* kern;
