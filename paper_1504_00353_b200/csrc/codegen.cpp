@@ -42,7 +42,7 @@ struct Spec {
     std::vector<uint8_t> mask;
     int W = 1024;   // warp subtree size for CTA mode
     int T = 512;    // threads per CTA in CTA mode
-    int warps = 4;  // frames (warps) per CTA in warp mode
+    int fpc_max = 16;  // most lockstep frames (warps) per CTA in the throughput variant
 };
 
 struct Emitter {
@@ -165,8 +165,8 @@ struct CtaEmitter {
     void sub_call(int id, const std::string& src) {
         std::string fname = "sub" + std::to_string(n_subs++);
         emit_warp_sub(subs, t, id, fname);
-        body << "        if (threadIdx.x < 32) " << fname << "<P>(" << src << ", beta);\n"
-             << "        group_sync<T>();\n";
+        body << "        if (gtid<T>() < 32) " << fname << "<P>(" << src << ", beta);\n"
+             << "        sync();\n";
     }
 
     void child(int id, const std::string& src) {
@@ -186,14 +186,14 @@ struct CtaEmitter {
             case Kind::Rate0:
                 return;
             case Kind::Rate1:
-                body << "        cR1<P, T, " << N_ << ">(" << src << ", " << B << ");\n        group_sync<T>();\n";
+                body << "        cR1<P, T, " << N_ << ">(" << src << ", " << B << ");\n        sync();\n";
                 return;
             case Kind::Rep:
                 body << "        cRep<P, T, " << N_ << ">(" << src << ", " << stage(n / 2) << ", " << B
-                     << ");\n        group_sync<T>();\n";
+                     << ");\n        sync();\n";
                 return;
             case Kind::Spc:
-                body << "        cSPC<P, T, " << N_ << ">(" << src << ", " << B << ");\n        group_sync<T>();\n";
+                body << "        cSPC<P, T, " << N_ << ">(" << src << ", " << B << ");\n        sync();\n";
                 return;
             case Kind::Split:
                 break;
@@ -203,17 +203,17 @@ struct CtaEmitter {
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
         if (l.kind == Kind::Rate0) {
-            body << "        cG0R<P, T, " << N_ << ", " << CL << ">(" << src << ", " << D << ");\n        group_sync<T>();\n";
+            body << "        cG0R<P, T, " << N_ << ", " << CL << ">(" << src << ", " << D << ");\n        sync();\n";
             child(v.right, D);
-            body << "        cComb0R<T, " << N_ << ">(" << B << ");\n        group_sync<T>();\n";
+            body << "        cComb0R<T, " << N_ << ">(" << B << ");\n        sync();\n";
             return;
         }
-        body << "        cF<P, T, " << N_ << ", " << CL << ">(" << src << ", " << D << ");\n        group_sync<T>();\n";
+        body << "        cF<P, T, " << N_ << ", " << CL << ">(" << src << ", " << D << ");\n        sync();\n";
         child(v.left, D);
         if (r.kind == Kind::Rate0) return;
-        body << "        cG<P, T, " << N_ << ", " << CL << ", false>(" << src << ", " << D << ", " << B << ");\n        group_sync<T>();\n";
+        body << "        cG<P, T, " << N_ << ", " << CL << ", false>(" << src << ", " << D << ", " << B << ");\n        sync();\n";
         child(v.right, D);
-        body << "        cComb<T, " << N_ << ">(" << B << ");\n        group_sync<T>();\n";
+        body << "        cComb<T, " << N_ << ">(" << B << ");\n        sync();\n";
     }
 };
 
@@ -241,9 +241,9 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     if (!cta_phase) {
         o << "    static constexpr int STAGE_ELEMS = 0;\n";
         emit_warp_sub(o, t, 0, "decode_root");
-        o << "    template <class P, int T, class ChanT>\n"
-          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, uint32_t* beta) {\n"
-          << "        if (threadIdx.x < 32) decode_root<P>(chan, beta);\n    }\n";
+        o << "    template <class P, int T, class ChanT, class SyncT>\n"
+          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, uint32_t* beta, const SyncT&) {\n"
+          << "        if (gtid<T>() < 32) decode_root<P>(chan, beta);\n    }\n";
     } else {
         std::ostringstream body, subs;
         CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, 0};
@@ -255,8 +255,9 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         ce.cta(0, "chan");
         o << "    static constexpr int STAGE_ELEMS = " << acc << ";\n";
         o << subs.str();
-        o << "    template <class P, int T, class ChanT>\n"
-          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, uint32_t* beta) {\n"
+        o << "    template <class P, int T, class ChanT, class SyncT>\n"
+          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, uint32_t* beta,\n"
+          << "                                 const SyncT& sync) {\n"
           << body.str() << "    }\n";
     }
     o << "};\n\n}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
@@ -266,17 +267,30 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         const char* prof;
         int T;
         bool chan_smem;
+        int fpc;
     };
     auto bytes = [&](const char* prof) { return sp.N * (std::string(prof) == "PF32" ? 4 : 1); };
+    // Throughput variant: as many lockstep warps (frames) per CTA as the shared memory of one
+    // SM holds, at most 16 (same formula as FrameLayout::PER_FRAME).
+    auto a16 = [](int x) { return (x + 15) & ~15; };
+    auto fpc = [&](const char* prof, bool chan_smem) {
+        const int s = std::string(prof) == "PF32" ? 4 : 1;
+        const int stages = a16(std::max(0, cta_phase ? sp.N - W : 0) * s);
+        const int outw = a16((sp.K + 31) / 32 * 4);
+        const int per = (chan_smem ? 2 * a16(sp.N * s) : 0) + stages + a16(std::max(1, sp.N / 32) * 4) +
+                        (stages >= outw ? 0 : outw) + 16;
+        return std::max(1, std::min(sp.fpc_max, (220 * 1024) / per));
+    };
+    const bool cs_f = 2 * bytes("PF32") <= 16384, cs_i = 2 * bytes("PI8") <= 16384;
     std::vector<V> vars = {
-        {"tp_f32", "PF32", 32, 2 * bytes("PF32") <= 16384},
-        {"tp_i8", "PI8", 32, 2 * bytes("PI8") <= 16384},
-        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768},
-        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768},
+        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f)},
+        {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i)},
+        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1},
+        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1},
     };
     for (auto& v : vars) {
         const std::string targs = std::string("pd::") + v.prof + ", " + C + ", " + std::to_string(v.T) + ", " +
-                                  (v.chan_smem ? "true" : "false");
+                                  std::to_string(v.fpc) + ", " + (v.chan_smem ? "true" : "false");
         o << "extern const void* const polar_kern_" << sp.name << "_" << v.tag << " = (const void*)&pd::k_frame<"
           << targs << ">;\n"
           << "extern const unsigned polar_smem_" << sp.name << "_" << v.tag << " = pd::FrameLayout<" << targs
@@ -295,7 +309,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                 << code_hash(sp.N, sp.K, sp.mask.data()) << "ull, " << ops.size() << ", " << W;
     for (auto& v : vars)
         reg_entries << ", {&polar_kern_" << sp.name << "_" << v.tag << ", &polar_smem_" << sp.name << "_" << v.tag
-                    << ", " << v.T << "}";
+                    << ", " << v.T << ", " << v.fpc << "}";
     reg_entries << ", \"" << sched << "\"},\n";
 }
 
@@ -350,7 +364,7 @@ int main(int argc, char** argv) {
         while (ls >> opt) {
             if (opt.rfind("W=", 0) == 0) sp.W = std::atoi(opt.c_str() + 2);
             else if (opt.rfind("T=", 0) == 0) sp.T = std::atoi(opt.c_str() + 2);
-            else if (opt.rfind("WARPS=", 0) == 0) sp.warps = std::atoi(opt.c_str() + 6);
+            else if (opt.rfind("FPC=", 0) == 0) sp.fpc_max = std::atoi(opt.c_str() + 4);
         }
         specs.push_back(sp);
     }

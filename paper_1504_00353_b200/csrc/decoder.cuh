@@ -53,6 +53,9 @@ PD_INLINE uint32_t h2max(uint32_t a, uint32_t b) {
 }
 
 PD_INLINE unsigned lane_id() { return threadIdx.x & 31u; }
+// Index of the thread in its frame group of T threads (T = 32: the lane).
+template <int T>
+PD_INLINE int gtid() { return T == 32 ? (int)(threadIdx.x & 31u) : (int)threadIdx.x; }
 
 __host__ __device__ constexpr int slots(int n) { return n >= 32 ? n / 32 : 1; }
 __host__ __device__ constexpr uint32_t low_mask(int n) { return n >= 32 ? 0xffffffffu : ((1u << n) - 1u); }
@@ -430,7 +433,7 @@ template <class P, int T, int n, bool CLAMP, class TS>
 PD_INLINE void cF(const TS* __restrict__ src, typename P::st_t* __restrict__ dst) {
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
 #pragma unroll 2
-    for (int i = CE * threadIdx.x; i < H; i += CE * T) {
+    for (int i = CE * gtid<T>(); i < H; i += CE * T) {
         Chunk<P, CE> a, b;
         if constexpr (sizeof(typename P::st_t) == 1) {
             a.load(src + i, CLAMP);
@@ -447,7 +450,7 @@ template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, class TS>
 PD_INLINE void cG(const TS* __restrict__ src, typename P::st_t* __restrict__ dst, const uint32_t* beta) {
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
 #pragma unroll 2
-    for (int i = CE * threadIdx.x; i < H; i += CE * T) {
+    for (int i = CE * gtid<T>(); i < H; i += CE * T) {
         Chunk<P, CE> a, b;
         if constexpr (sizeof(typename P::st_t) == 1) {
             a.load(src + i, CLAMP);
@@ -467,56 +470,55 @@ PD_INLINE void cG0R(const TS* __restrict__ src, typename P::st_t* __restrict__ d
 }
 template <class P, int T, int n, class TS>
 PD_INLINE void cR1(const TS* __restrict__ src, uint32_t* beta) {
-    for (int k = threadIdx.x >> 5; k < n / 32; k += T / 32) {
+    for (int k = (gtid<T>() >> 5); k < n / 32; k += T / 32) {
         const uint32_t w = __ballot_sync(FULL, P::hd(P::ld(src[32 * k + lane_id()])));
         if (lane_id() == 0) beta[k] = w;
     }
 }
 // Repetition at CTA scope.  f32: pairwise-halving order (reading C13) run in
-// place on `scratch` (the free child stage of size n/2); int8: exact integer sum.
+// place on `scratch` (the free child stage of size n/2); int8: exact integer sum.  A lone
+// warp (T = 32, possibly one of several frame groups of a CTA) reduces with shuffles only.
 template <class P, int T, int n, class TS>
 PD_INLINE void cRep(const TS* __restrict__ src, typename P::st_t* scratch, uint32_t* beta) {
-    __shared__ int red[T / 32];
-    __shared__ int decision;
-    const int warp = threadIdx.x >> 5;
+    using A = typename P::acc_t;
+    bool decision;
     if constexpr (P::kExactSum) {
-        typename P::acc_t s = 0;
-        for (int i = threadIdx.x; i < n; i += T) s = P::add(s, P::acc(P::ld(src[i])));
+        A s = 0;
+        for (int i = gtid<T>(); i < n; i += T) s = P::add(s, P::acc(P::ld(src[i])));
 #pragma unroll
         for (int o = 16; o; o >>= 1) s = P::add(s, __shfl_xor_sync(FULL, s, o));
-        if (lane_id() == 0) red[warp] = (int)s;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            long long tot = 0;
-            for (int w = 0; w < T / 32; ++w) tot += red[w];
-            decision = tot < 0;
+        if constexpr (T == 32) {
+            decision = P::acc_neg(s);
+        } else {
+            __shared__ A red[T / 32];
+            if (lane_id() == 0) red[gtid<T>() >> 5] = s;
+            __syncthreads();
+            A tot = 0;  // exact: integer-valued, |sum| < 2^24
+            for (int w = 0; w < T / 32; ++w) tot = P::add(tot, red[w]);
+            decision = P::acc_neg(tot);
         }
     } else {
-        for (int i = threadIdx.x; i < n / 2; i += T) scratch[i] = P::st(P::add(P::ld(src[i]), P::ld(src[i + n / 2])));
-        __syncthreads();
+        for (int i = gtid<T>(); i < n / 2; i += T) scratch[i] = P::st(P::add(P::ld(src[i]), P::ld(src[i + n / 2])));
+        group_sync<T>();
         for (int m = n / 2; m > 32; m /= 2) {
-            for (int i = threadIdx.x; i < m / 2; i += T) scratch[i] = P::add(scratch[i], scratch[i + m / 2]);
-            __syncthreads();
+            for (int i = gtid<T>(); i < m / 2; i += T) scratch[i] = P::add(scratch[i], scratch[i + m / 2]);
+            group_sync<T>();
         }
-        if (warp == 0) {
-            typename P::acc_t t = scratch[lane_id()];
+        A t = scratch[lane_id()];  // every warp reduces the last 32 values the same way
 #pragma unroll
-            for (int o = 16; o; o >>= 1) t = P::add(t, __shfl_down_sync(FULL, t, o));
-            if (lane_id() == 0) decision = P::acc_neg(t);
-        }
+        for (int o = 16; o; o >>= 1) t = P::add(t, __shfl_down_sync(FULL, t, o));
+        decision = __shfl_sync(FULL, (int)P::acc_neg(t), 0) != 0;
     }
-    __syncthreads();
     const uint32_t w = decision ? FULL : 0u;
-    for (int k = threadIdx.x; k < n / 32; k += T) beta[k] = w;
+    for (int k = gtid<T>(); k < n / 32; k += T) beta[k] = w;
+    group_sync<T>();
 }
 
 // SPC at CTA scope: ballot hard decisions per word, parity of all, flip the
 // lowest-index least-magnitude bit when odd (reading C10); key = (|alpha| << 32) | index.
 template <class P, int T, int n, class TS>
 PD_INLINE void cSPC(const TS* __restrict__ src, uint32_t* beta) {
-    __shared__ unsigned long long red[T / 32];
-    __shared__ uint32_t par[T / 32];
-    const int warp = threadIdx.x >> 5;
+    const int warp = (gtid<T>() >> 5);
     unsigned long long best = ~0ull;
     uint32_t p = 0;
     for (int k = warp; k < n / 32; k += T / 32) {
@@ -532,33 +534,35 @@ PD_INLINE void cSPC(const TS* __restrict__ src, uint32_t* beta) {
         const unsigned long long other = __shfl_xor_sync(FULL, best, o);
         best = other < best ? other : best;
     }
-    if (lane_id() == 0) {
-        red[warp] = best;
-        par[warp] = p;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long b = ~0ull;
-        uint32_t q = 0;
+    if constexpr (T > 32) {
+        __shared__ unsigned long long red[T / 32];
+        __shared__ uint32_t par[T / 32];
+        if (lane_id() == 0) {
+            red[warp] = best;
+            par[warp] = p;
+        }
+        __syncthreads();
+        p = 0;
         for (int w = 0; w < T / 32; ++w) {
-            b = red[w] < b ? red[w] : b;
-            q ^= par[w];
-        }
-        if (q) {
-            const uint32_t idx = (uint32_t)b;
-            beta[idx >> 5] ^= 1u << (idx & 31);
+            best = red[w] < best ? red[w] : best;
+            p ^= par[w];
         }
     }
-    __syncthreads();
+    group_sync<T>();
+    if (gtid<T>() == 0 && p) {
+        const uint32_t idx = (uint32_t)best;
+        beta[idx >> 5] ^= 1u << (idx & 31);
+    }
+    group_sync<T>();
 }
 
 template <int T, int n>
 PD_INLINE void cComb(uint32_t* beta) {
-    for (int k = threadIdx.x; k < n / 64; k += T) beta[k] ^= beta[k + n / 64];
+    for (int k = gtid<T>(); k < n / 64; k += T) beta[k] ^= beta[k + n / 64];
 }
 template <int T, int n>
 PD_INLINE void cComb0R(uint32_t* beta) {
-    for (int k = threadIdx.x; k < n / 64; k += T) beta[k] = beta[k + n / 64];
+    for (int k = gtid<T>(); k < n / 64; k += T) beta[k] = beta[k + n / 64];
 }
 
 // ----------------------------------------------------------------------- frame output
@@ -588,9 +592,9 @@ PD_INLINE void gather_info(const uint32_t* beta, const uint32_t* __restrict__ ta
                            uint32_t* __restrict__ out) {
     constexpr int NB = N >= 32 ? N / 32 : 1;
     constexpr int NWK = (K + 31) / 32;
-    for (int q = threadIdx.x; q < NWK; q += T) stg[q] = 0;
+    for (int q = gtid<T>(); q < NWK; q += T) stg[q] = 0;
     group_sync<T>();
-    for (int k = threadIdx.x; k < NB; k += T) {
+    for (int k = gtid<T>(); k < NB; k += T) {
         const uint32_t m = __ldg(tab + k);
         if (!m) continue;
         const uint32_t p = __ldg(tab + NB + k);
@@ -600,7 +604,7 @@ PD_INLINE void gather_info(const uint32_t* beta, const uint32_t* __restrict__ ta
         if (sh && sh + __popc(m) > 32) atomicOr(stg + (p >> 5) + 1, r >> (32 - sh));
     }
     group_sync<T>();
-    for (int q = threadIdx.x; q < NWK; q += T) out[q] = stg[q];
+    for (int q = gtid<T>(); q < NWK; q += T) out[q] = stg[q];
 }
 
 // --------------------------------------------------------------- TMA bulk ingest helpers

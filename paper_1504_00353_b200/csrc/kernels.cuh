@@ -26,7 +26,19 @@ PD_INLINE void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-template <class P, class C, int T, bool CHAN_SMEM>
+// Op-boundary barrier of a frame group.  Latency variant: the whole CTA.  Throughput variant:
+// all active warps of the CTA (named barrier 1), so that the FPC warps, each decoding its
+// own frame through the same unrolled code, stay in lockstep and share instruction fetch.
+template <int T>
+struct OpSync {
+    uint32_t threads;
+    PD_INLINE void operator()() const {
+        if constexpr (T > 32) __syncthreads();
+        else asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
+    }
+};
+
+template <class P, class C, int T, int FPC, bool CHAN_SMEM>
 struct FrameLayout {
     using in_t = typename P::in_t;
     using st_t = typename P::st_t;
@@ -40,21 +52,26 @@ struct FrameLayout {
     // output staging words: the stage area is free after the decode when it is large enough
     static constexpr int OUTW = align16((C::K + 31) / 32 * 4);
     static constexpr int STG = STAGES >= OUTW ? 0 : OUTW;
-    static constexpr int SMEM = NBUF * BUF + STAGES + BETA + STG + 16;
+    static constexpr int PER_FRAME = NBUF * BUF + STAGES + BETA + STG + 16;
+    static constexpr int SMEM = FPC * PER_FRAME;
 };
 
-template <class P, class C, int T, bool CHAN_SMEM>
-__global__ void __launch_bounds__(T)
+// FPC frame groups of T threads per CTA (FPC > 1 only with T = 32).
+template <class P, class C, int T, int FPC, bool CHAN_SMEM>
+__global__ void __launch_bounds__(T * FPC)
     k_frame(const void* __restrict__ llr_, long long n_frames, uint32_t* __restrict__ out,
             const uint32_t* __restrict__ gtab) {
-    using L = FrameLayout<P, C, T, CHAN_SMEM>;
+    static_assert(FPC == 1 || T == 32, "");
+    using L = FrameLayout<P, C, T, FPC, CHAN_SMEM>;
     using in_t = typename P::in_t;
     using st_t = typename P::st_t;
     constexpr int N = C::N;
     constexpr int NWK = (C::K + 31) / 32;
     constexpr bool TMA = CHAN_SMEM && L::kBulk;
     constexpr bool DBL = L::NBUF > 1;
-    extern __shared__ __align__(128) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem_all[];
+    const int grp = FPC > 1 ? (int)(threadIdx.x >> 5) : 0;
+    unsigned char* const smem = smem_all + grp * L::PER_FRAME;
     in_t* const buf0 = (in_t*)smem;
     in_t* const buf1 = (in_t*)(smem + (DBL ? L::BUF : 0));
     st_t* const stages = (st_t*)(smem + L::NBUF * L::BUF);
@@ -62,49 +79,56 @@ __global__ void __launch_bounds__(T)
     uint32_t* const stg = (uint32_t*)(L::STG ? smem + L::NBUF * L::BUF + L::STAGES + L::BETA : (unsigned char*)stages);
     uint64_t* const bar = (uint64_t*)(smem + L::NBUF * L::BUF + L::STAGES + L::BETA + L::STG);
     const in_t* llr = (const in_t*)llr_;
+    const unsigned tid = FPC > 1 ? (threadIdx.x & 31u) : threadIdx.x;  // thread index in its group
+    const bool leader = tid == 0;
 
-    long long f = blockIdx.x;
-    const long long stride = gridDim.x;
+    // frames of round r: (r * gridDim.x + blockIdx.x) * FPC + grp
+    const long long stride = (long long)gridDim.x * FPC;
+    long long f = (long long)blockIdx.x * FPC + grp;
     if constexpr (TMA) {
-        if (threadIdx.x == 0) {
+        if (leader) {
             mbar_init(bar, 1);
             mbar_init(bar + 1, 1);
             fence_barrier_init();
             if (f < n_frames) tma_load_1d(buf0, llr + f * N, L::FRAME_BYTES, bar);
         }
-        group_sync<T>();
+        __syncwarp();
+        if constexpr (T > 32) __syncthreads();
     }
     for (int it = 0; f < n_frames; f += stride, ++it) {
+        // warps of this round that have a frame: they alone take part in the op barriers
+        const long long base = f - grp;
+        const OpSync<T> sync{(uint32_t)(32 * (FPC > 1 ? (int)min((long long)FPC, n_frames - base) : 1))};
         const long long nf = f + stride;
         const in_t* chan;
         if constexpr (TMA) {
             in_t* cur = (DBL && (it & 1)) ? buf1 : buf0;
-            if (DBL && threadIdx.x == 0 && nf < n_frames) {
-                // buffer (it+1)&1 was last read in iteration it-1, which ended with a barrier
+            if (DBL && leader && nf < n_frames) {
+                // buffer (it+1)&1 was last read in round it-1, which ended with a barrier
                 fence_proxy_async();
                 tma_load_1d((it & 1) ? buf0 : buf1, llr + nf * N, L::FRAME_BYTES, bar + ((it + 1) & 1));
             }
             mbar_wait(bar + (DBL ? (it & 1) : 0), DBL ? ((it >> 1) & 1) : (it & 1));
             chan = cur;
         } else if constexpr (CHAN_SMEM) {
-            for (int i = threadIdx.x; i < N; i += T) buf0[i] = llr[f * N + i];
-            group_sync<T>();
+            for (int i = tid; i < N; i += T) buf0[i] = llr[f * N + i];
+            sync();
             chan = buf0;
         } else {
-            if (L::kBulk && threadIdx.x == 0 && nf < n_frames) prefetch_l2(llr + nf * N, L::FRAME_BYTES);
+            if (L::kBulk && leader && nf < n_frames) prefetch_l2(llr + nf * N, L::FRAME_BYTES);
             chan = llr + f * N;
         }
         if constexpr (C::STAGE_ELEMS > 0) {
-            for (int k = threadIdx.x; k < N / 32; k += T) beta[k] = 0;
-            group_sync<T>();
+            for (int k = tid; k < N / 32; k += T) beta[k] = 0;
+            sync();
         }
-        C::template decode<P, T>(chan, stages, beta);
-        group_sync<T>();
+        C::template decode<P, T>(chan, stages, beta, sync);
+        sync();
         gather_info<N, C::K, T>(beta, gtab, stg, out + f * NWK);
-        group_sync<T>();
+        sync();
         if constexpr (TMA && !DBL) {
             // single buffer: the next frame's copy starts once every thread is done with this one
-            if (threadIdx.x == 0 && nf < n_frames) {
+            if (leader && nf < n_frames) {
                 fence_proxy_async();
                 tma_load_1d(buf0, llr + nf * N, L::FRAME_BYTES, bar);
             }

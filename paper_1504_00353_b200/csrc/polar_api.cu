@@ -101,7 +101,8 @@ static polar_status init_device(polar_code* h) {
     for (int i = 0; i < 4; ++i) {
         const void* k = *vs[i]->kern;
         CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*vs[i]->smem));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ[i], k, (int)vs[i]->threads, *vs[i]->smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ[i], k, (int)(vs[i]->threads * vs[i]->frames),
+                                                               *vs[i]->smem));
         if (h->occ[i] < 1) return fail(POLAR_ERR_CUDA, "decoder kernel variant %d cannot be resident", i);
     }
     std::vector<uint16_t> pos;
@@ -243,11 +244,11 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     const void* kern = *v.kern;
     const unsigned smem = *v.smem;
     const int64_t resident = (int64_t)h->occ[vi] * h->n_sm;
-    const unsigned grid = (unsigned)std::min<int64_t>(n, resident);
+    const unsigned grid = (unsigned)std::min<int64_t>((n + v.frames - 1) / v.frames, resident);
     long long nn = (long long)n;
     const uint32_t* gtab = h->d_gtab;
     void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab};
-    CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(v.threads), args, smem, s));
+    CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(v.threads * v.frames), args, smem, s));
     return POLAR_OK;
 }
 

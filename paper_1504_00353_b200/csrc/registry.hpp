@@ -12,7 +12,8 @@ namespace polar {
 struct Variant {
     const void* const* kern;
     const unsigned* smem;  // dynamic shared memory per CTA
-    uint32_t threads;      // threads per CTA = threads per frame
+    uint32_t threads;      // threads per frame group
+    uint32_t frames;       // frame groups (frames decoded concurrently) per CTA
 };
 
 struct RegistryEntry {
