@@ -16,6 +16,7 @@
 #include <iostream>
 #include <algorithm>
 #include <map>
+#include <set>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -43,24 +44,49 @@ struct Spec {
     int W = 1024;   // warp subtree size for CTA mode
     int T = 512;    // threads per CTA in CTA mode
     int fpc_max = 16;  // most lockstep frames (warps) per CTA in the throughput variant
+    std::set<int> dedup = {16, 32, 64};  // sizes of subtrees shared as noinline functions
+};
+
+// Distinct small-subtree patterns emitted once as __noinline__ device functions, so that the
+// unrolled code of a large code stays small enough for the instruction caches: at (32768,29492)
+// the 120 size-32 split subtrees have 28 distinct frozen patterns.
+struct SharedFns {
+    const std::vector<uint8_t>& mask;
+    std::set<int> sizes;                 // node sizes that are deduplicated
+    std::map<std::string, std::string> by_key;
+    std::ostringstream defs;
 };
 
 struct Emitter {
     const Tree& t;
     std::ostringstream& o;
+    SharedFns* sh = nullptr;
     int next_mask = 0;
     std::string ind = "        ";
+    int body_root = -1;  // the node whose shared function body is being emitted
 
     std::string mask_name() { return "m" + std::to_string(next_mask++); }
 
     // Emit the warp-scope decode of node id (size n) at bit offset off relative to the
     // subtree root.  src: the C++ expression of its LLR source.  Returns the name of the
     // uniform mask holding its beta when n <= 32, "" when beta was written into bw.
-    std::string warp(int id, int off, const std::string& src) {
+    std::string shared_fn(int id);
+
+    std::string warp(int id, int off, const std::string& src, const std::string& src_arr = "") {
         const Node& v = t.nodes[id];
         const int n = v.n;
         const int s0 = off / 32;
         const std::string N_ = std::to_string(n), S0 = std::to_string(s0);
+        if (sh && v.kind == Kind::Split && !src_arr.empty() && sh->sizes.count(n) && id != body_root) {
+            const std::string fn = shared_fn(id);
+            std::string args;
+            for (int j = 0; j < (n >= 32 ? n / 32 : 1); ++j) args += (j ? ", " : "") + src_arr + "[" + std::to_string(j) + "]";
+            const std::string m = mask_name();
+            o << ind << "const uint32_t " << m << " = " << fn << "<P>(" << args << ");\n";
+            if (n <= 32) return m;
+            o << ind << "bw |= (uint64_t)" << m << " << " << s0 << ";\n";
+            return "";
+        }
         switch (v.kind) {
             case Kind::Rate0:
                 return n <= 32 ? "0u" : "";
@@ -95,11 +121,12 @@ struct Emitter {
         const std::string H = std::to_string(h);
         const std::string child = "r" + std::to_string(ilog2(h));
         const std::string csrc = "RegSrc<P>{" + child + "}";
+        // children read the register stage `child`
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
         if (l.kind == Kind::Rate0) {
             o << ind << "wG0R<P, " << N_ << ">(" << src << ", " << child << ");\n";
-            std::string mr = warp(v.right, off + h, csrc);
+            std::string mr = warp(v.right, off + h, csrc, child);
             if (n <= 32) {
                 std::string m = mask_name();
                 o << ind << "const uint32_t " << m << " = " << mr << " | (" << mr << " << " << H << ");\n";
@@ -110,12 +137,12 @@ struct Emitter {
             return "";
         }
         o << ind << "wF<P, " << N_ << ">(" << src << ", " << child << ");\n";
-        std::string ml = warp(v.left, off, csrc);
+        std::string ml = warp(v.left, off, csrc, child);
         if (h == 32 && ml != "0u") o << ind << "wDeposit<" << s0 << ">(bw, " << ml << ");\n";
         if (r.kind == Kind::Rate0) return n <= 32 ? ml : "";
         o << ind << "wG<P, " << N_ << ", " << S0 << ">(" << src << ", " << child << ", bw, "
           << (n <= 32 ? ml : std::string("0u")) << ");\n";
-        std::string mr = warp(v.right, off + h, csrc);
+        std::string mr = warp(v.right, off + h, csrc, child);
         if (n <= 32) {
             std::string m = mask_name();
             o << ind << "const uint32_t " << m << " = (" << ml << " ^ " << mr << ") | (" << mr << " << " << H
@@ -128,8 +155,38 @@ struct Emitter {
     }
 };
 
+// Emit (once per distinct frozen pattern) a __noinline__ function decoding the split node id
+// from its stage values passed in registers; it returns the node's beta: the warp-uniform
+// mask for n <= 32, else the lane's n/32 slot bits.
+std::string Emitter::shared_fn(int id) {
+    const Node& v = t.nodes[id];
+    const int n = v.n;
+    std::string key = std::to_string(n) + ":";
+    for (int i = v.off; i < v.off + n; ++i) key += sh->mask[i] ? '1' : '0';
+    auto it = sh->by_key.find(key);
+    if (it != sh->by_key.end()) return it->second;
+    const std::string fn = "sf" + std::to_string(n) + "_" + std::to_string(sh->by_key.size());
+    std::ostringstream body;
+    Emitter e{t, body, sh};
+    e.body_root = id;
+    const int S = n >= 32 ? n / 32 : 1;
+    for (int k = ilog2(n) - 1; k >= 0; --k)
+        body << "    V r" << k << "[" << ((1 << k) >= 32 ? (1 << k) / 32 : 1) << "];\n";
+    body << "    uint64_t bw = 0;\n    (void)bw;\n";
+    e.ind = "    ";
+    std::string m = e.warp(id, 0, "RegSrc<P>{in}", "in");
+    // the name is reserved only after the body: nested patterns get their definitions first
+    sh->by_key[key] = fn;
+    sh->defs << "template <class P>\n__device__ __noinline__ uint32_t " << fn << "(";
+    for (int j = 0; j < S; ++j) sh->defs << (j ? ", " : "") << "typename P::v_t a" << j;
+    sh->defs << ") {\n    using V = typename P::v_t;\n    V in[" << S << "] = {";
+    for (int j = 0; j < S; ++j) sh->defs << (j ? ", " : "") << "a" << j;
+    sh->defs << "};\n" << body.str() << "    return " << (n <= 32 ? m : std::string("(uint32_t)bw")) << ";\n}\n\n";
+    return fn;
+}
+
 // A warp subtree function: root node id, whose input LLRs are at `src` (shared memory).
-void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::string& fname) {
+void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::string& fname, SharedFns* sh) {
     const Node& v = t.nodes[id];
     const int R = v.n;
     o << "    template <class P, class SrcT>\n"
@@ -141,7 +198,7 @@ void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::stri
         o << "        V r" << k << "[" << (size >= 32 ? size / 32 : 1) << "];\n";
     }
     o << "        uint64_t bw = 0;\n        (void)bw;\n";
-    Emitter e{t, o};
+    Emitter e{t, o, sh};
     std::string m = e.warp(id, 0, "src");
     if (R >= 64) {
         o << "        wStoreBeta<" << R << ">(bw, beta + " << v.off / 32 << ");\n";
@@ -159,12 +216,13 @@ struct CtaEmitter {
     int W, T, N;
     std::map<int, int> stage_off;  // stage size -> element offset
     int n_subs = 0;
+    SharedFns* sh = nullptr;
 
     std::string stage(int m) { return "(stages + " + std::to_string(stage_off.at(m)) + ")"; }
 
     void sub_call(int id, const std::string& src) {
         std::string fname = "sub" + std::to_string(n_subs++);
-        emit_warp_sub(subs, t, id, fname);
+        emit_warp_sub(subs, t, id, fname, sh);
         body << "        if (gtid<T>() < 32) " << fname << "<P>(" << src << ", beta);\n"
              << "        sync();\n";
     }
@@ -230,23 +288,21 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     const int W = std::min(sp.N, sp.W);
     const bool cta_phase = sp.N > W;
     const int t_lat = cta_phase ? sp.T : 32;
+    SharedFns sh{sp.mask, sp.dedup, {}, {}};
     std::ostringstream o;
-    o << "// Generated by codegen.cpp for code " << sp.name << " (N=" << sp.N << ", K=" << sp.K
-      << ", " << ops.size() << " Fast-SSC ops, W=" << W << "). Do not edit.\n"
-      << "#include \"kernels.cuh\"\n\nnamespace pd {\nnamespace code_" << sp.name << " {\n\n"
-      << "struct Code {\n"
+    o << "struct Code {\n"
       << "    static constexpr int N = " << sp.N << ";\n"
       << "    static constexpr int K = " << sp.K << ";\n"
       << "    static constexpr int W = " << W << ";\n";
     if (!cta_phase) {
         o << "    static constexpr int STAGE_ELEMS = 0;\n";
-        emit_warp_sub(o, t, 0, "decode_root");
+        emit_warp_sub(o, t, 0, "decode_root", &sh);
         o << "    template <class P, int T, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, uint32_t* beta, const SyncT&) {\n"
           << "        if (gtid<T>() < 32) decode_root<P>(chan, beta);\n    }\n";
     } else {
         std::ostringstream body, subs;
-        CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, 0};
+        CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, 0, &sh};
         int acc = 0;
         for (int m = sp.N / 2; m >= W; m /= 2) {
             ce.stage_off[m] = acc;
@@ -261,6 +317,17 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
           << body.str() << "    }\n";
     }
     o << "};\n\n}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
+    {
+        std::ostringstream head;
+        head << "// Generated by codegen.cpp for code " << sp.name << " (N=" << sp.N << ", K=" << sp.K << ", "
+             << ops.size() << " Fast-SSC ops, W=" << W << ", " << sh.by_key.size()
+             << " shared subtree functions). Do not edit.\n"
+             << "#include \"kernels.cuh\"\n\nnamespace pd {\nnamespace code_" << sp.name << " {\n\n"
+             << sh.defs.str();
+        const std::string rest = o.str();
+        o.str("");
+        o << head.str() << rest;
+    }
     const std::string C = "pd::code_" + sp.name + "::Code";
     struct V {
         const char* tag;
@@ -365,6 +432,13 @@ int main(int argc, char** argv) {
             if (opt.rfind("W=", 0) == 0) sp.W = std::atoi(opt.c_str() + 2);
             else if (opt.rfind("T=", 0) == 0) sp.T = std::atoi(opt.c_str() + 2);
             else if (opt.rfind("FPC=", 0) == 0) sp.fpc_max = std::atoi(opt.c_str() + 4);
+            else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
+                sp.dedup.clear();
+                std::stringstream ds(opt.substr(6));
+                std::string tok;
+                while (std::getline(ds, tok, ','))
+                    if (tok != "none") sp.dedup.insert(std::atoi(tok.c_str()));
+            }
         }
         specs.push_back(sp);
     }
