@@ -44,7 +44,8 @@ struct Spec {
     int W = 1024;   // warp subtree size for CTA mode
     int T = 512;    // threads per CTA in CTA mode
     int fpc_max = 16;  // most lockstep frames (warps) per CTA in the throughput variant
-    std::set<int> dedup = {16, 32, 64};  // sizes of subtrees shared as noinline functions
+    std::set<int> dedup;  // sizes of subtrees shared as noinline functions (DEDUP=16,32,..)
+    int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
 };
 
 // Distinct small-subtree patterns emitted once as __noinline__ device functions, so that the
@@ -214,11 +215,16 @@ struct CtaEmitter {
     std::ostringstream& body;   // decode_cta body
     std::ostringstream& subs;   // warp subtree functions
     int W, T, N;
-    std::map<int, int> stage_off;  // stage size -> element offset
+    std::map<int, int> stage_off;  // stage size -> element offset, all stages in shared memory
+    std::map<int, int> soff, goff;  // split layout (GTOP): shared-memory part, global part
     int n_subs = 0;
     SharedFns* sh = nullptr;
 
-    std::string stage(int m) { return "(stages + " + std::to_string(stage_off.at(m)) + ")"; }
+    // GTOP (template flag of decode): the largest stages live in per-frame global scratch.
+    std::string stage(int m) {
+        if (goff.count(m)) return "(GTOP ? gst + " + std::to_string(goff.at(m)) + " : stages + " + std::to_string(stage_off.at(m)) + ")";
+        return "(stages + (GTOP ? " + std::to_string(soff.at(m)) + " : " + std::to_string(stage_off.at(m)) + "))";
+    }
 
     void sub_call(int id, const std::string& src) {
         std::string fname = "sub" + std::to_string(n_subs++);
@@ -295,25 +301,36 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
       << "    static constexpr int K = " << sp.K << ";\n"
       << "    static constexpr int W = " << W << ";\n";
     if (!cta_phase) {
-        o << "    static constexpr int STAGE_ELEMS = 0;\n";
+        o << "    static constexpr int STAGE_ELEMS = 0;\n    static constexpr int STAGE_ELEMS_SMEM = 0;\n"
+          << "    static constexpr int GSTAGE_ELEMS = 0;\n";
         emit_warp_sub(o, t, 0, "decode_root", &sh);
-        o << "    template <class P, int T, class ChanT, class SyncT>\n"
-          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, uint32_t* beta, const SyncT&) {\n"
+        o << "    template <class P, int T, bool GTOP, class ChanT, class SyncT>\n"
+          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, typename P::st_t*, uint32_t* beta, const SyncT&) {\n"
           << "        if (gtid<T>() < 32) decode_root<P>(chan, beta);\n    }\n";
     } else {
         std::ostringstream body, subs;
-        CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, 0, &sh};
-        int acc = 0;
+        CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, {}, {}, 0, &sh};
+        int acc = 0, sacc = 0, gacc = 0;
+        const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         for (int m = sp.N / 2; m >= W; m /= 2) {
             ce.stage_off[m] = acc;
             acc += m;
+            if (m >= gs) {
+                ce.goff[m] = gacc;
+                gacc += m;
+            } else {
+                ce.soff[m] = sacc;
+                sacc += m;
+            }
         }
         ce.cta(0, "chan");
-        o << "    static constexpr int STAGE_ELEMS = " << acc << ";\n";
+        o << "    static constexpr int STAGE_ELEMS = " << acc << ";\n"
+          << "    static constexpr int STAGE_ELEMS_SMEM = " << sacc << ";  // GTOP layout\n"
+          << "    static constexpr int GSTAGE_ELEMS = " << gacc << ";\n";
         o << subs.str();
-        o << "    template <class P, int T, class ChanT, class SyncT>\n"
-          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, uint32_t* beta,\n"
-          << "                                 const SyncT& sync) {\n"
+        o << "    template <class P, int T, bool GTOP, class ChanT, class SyncT>\n"
+          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
+          << "                                 uint32_t* beta, const SyncT& sync) {\n"
           << body.str() << "    }\n";
     }
     o << "};\n\n}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
@@ -335,29 +352,38 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         int T;
         bool chan_smem;
         int fpc;
+        bool gtop;
     };
     auto bytes = [&](const char* prof) { return sp.N * (std::string(prof) == "PF32" ? 4 : 1); };
     // Throughput variant: as many lockstep warps (frames) per CTA as the shared memory of one
     // SM holds, at most 16 (same formula as FrameLayout::PER_FRAME).
     auto a16 = [](int x) { return (x + 15) & ~15; };
+    int g_elems = 0;
+    if (cta_phase) {
+        const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
+        for (int m = sp.N / 2; m >= W; m /= 2)
+            if (m >= gs) g_elems += m;
+    }
     auto fpc = [&](const char* prof, bool chan_smem) {
         const int s = std::string(prof) == "PF32" ? 4 : 1;
-        const int stages = a16(std::max(0, cta_phase ? sp.N - W : 0) * s);
+        const int stages = a16(std::max(0, cta_phase ? sp.N - W - g_elems : 0) * s);
         const int outw = a16((sp.K + 31) / 32 * 4);
         const int per = (chan_smem ? 2 * a16(sp.N * s) : 0) + stages + a16(std::max(1, sp.N / 32) * 4) +
                         (stages >= outw ? 0 : outw) + 16;
         return std::max(1, std::min(sp.fpc_max, (220 * 1024) / per));
     };
     const bool cs_f = 2 * bytes("PF32") <= 16384, cs_i = 2 * bytes("PI8") <= 16384;
+    const bool gt = g_elems > 0;
     std::vector<V> vars = {
-        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f)},
-        {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i)},
-        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1},
-        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1},
+        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f), gt},
+        {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i), gt},
+        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1, false},
+        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1, false},
     };
     for (auto& v : vars) {
         const std::string targs = std::string("pd::") + v.prof + ", " + C + ", " + std::to_string(v.T) + ", " +
-                                  std::to_string(v.fpc) + ", " + (v.chan_smem ? "true" : "false");
+                                  std::to_string(v.fpc) + ", " + (v.chan_smem ? "true" : "false") + ", " +
+                                  (v.gtop ? "true" : "false");
         o << "extern const void* const polar_kern_" << sp.name << "_" << v.tag << " = (const void*)&pd::k_frame<"
           << targs << ">;\n"
           << "extern const unsigned polar_smem_" << sp.name << "_" << v.tag << " = pd::FrameLayout<" << targs
@@ -376,7 +402,8 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                 << code_hash(sp.N, sp.K, sp.mask.data()) << "ull, " << ops.size() << ", " << W;
     for (auto& v : vars)
         reg_entries << ", {&polar_kern_" << sp.name << "_" << v.tag << ", &polar_smem_" << sp.name << "_" << v.tag
-                    << ", " << v.T << ", " << v.fpc << "}";
+                    << ", " << v.T << ", " << v.fpc << ", "
+                    << (v.gtop ? g_elems * (std::string(v.prof) == "PF32" ? 4 : 1) : 0) << "}";
     reg_entries << ", \"" << sched << "\"},\n";
 }
 
@@ -432,6 +459,7 @@ int main(int argc, char** argv) {
             if (opt.rfind("W=", 0) == 0) sp.W = std::atoi(opt.c_str() + 2);
             else if (opt.rfind("T=", 0) == 0) sp.T = std::atoi(opt.c_str() + 2);
             else if (opt.rfind("FPC=", 0) == 0) sp.fpc_max = std::atoi(opt.c_str() + 4);
+            else if (opt.rfind("GS=", 0) == 0) sp.gs = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();
                 std::stringstream ds(opt.substr(6));

@@ -38,7 +38,7 @@ struct OpSync {
     }
 };
 
-template <class P, class C, int T, int FPC, bool CHAN_SMEM>
+template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP>
 struct FrameLayout {
     using in_t = typename P::in_t;
     using st_t = typename P::st_t;
@@ -47,7 +47,7 @@ struct FrameLayout {
     // throughput warps double-buffer (prefetch the next frame), the latency CTA single-buffers
     static constexpr int NBUF = CHAN_SMEM ? (T == 32 ? 2 : 1) : 0;
     static constexpr int BUF = align16(FRAME_BYTES);
-    static constexpr int STAGES = align16(C::STAGE_ELEMS * (int)sizeof(st_t));
+    static constexpr int STAGES = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t));
     static constexpr int BETA = align16((C::N >= 32 ? C::N / 32 : 1) * 4);
     // output staging words: the stage area is free after the decode when it is large enough
     static constexpr int OUTW = align16((C::K + 31) / 32 * 4);
@@ -57,12 +57,14 @@ struct FrameLayout {
 };
 
 // FPC frame groups of T threads per CTA (FPC > 1 only with T = 32).
-template <class P, class C, int T, int FPC, bool CHAN_SMEM>
+// GTOP: the stages of size >= N/4 live in global scratch (L2-resident), one slot per frame
+// group of the persistent grid, so that more frames fit in shared memory per SM.
+template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP>
 __global__ void __launch_bounds__(T * FPC)
     k_frame(const void* __restrict__ llr_, long long n_frames, uint32_t* __restrict__ out,
-            const uint32_t* __restrict__ gtab) {
+            const uint32_t* __restrict__ gtab, void* __restrict__ gscratch) {
     static_assert(FPC == 1 || T == 32, "");
-    using L = FrameLayout<P, C, T, FPC, CHAN_SMEM>;
+    using L = FrameLayout<P, C, T, FPC, CHAN_SMEM, GTOP>;
     using in_t = typename P::in_t;
     using st_t = typename P::st_t;
     constexpr int N = C::N;
@@ -79,6 +81,7 @@ __global__ void __launch_bounds__(T * FPC)
     uint32_t* const stg = (uint32_t*)(L::STG ? smem + L::NBUF * L::BUF + L::STAGES + L::BETA : (unsigned char*)stages);
     uint64_t* const bar = (uint64_t*)(smem + L::NBUF * L::BUF + L::STAGES + L::BETA + L::STG);
     const in_t* llr = (const in_t*)llr_;
+    st_t* const gst = GTOP ? (st_t*)gscratch + ((long long)blockIdx.x * FPC + grp) * C::GSTAGE_ELEMS : nullptr;
     const unsigned tid = FPC > 1 ? (threadIdx.x & 31u) : threadIdx.x;  // thread index in its group
     const bool leader = tid == 0;
 
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(T * FPC)
             for (int k = tid; k < N / 32; k += T) beta[k] = 0;
             sync();
         }
-        C::template decode<P, T>(chan, stages, beta, sync);
+        C::template decode<P, T, GTOP>(chan, stages, gst, beta, sync);
         sync();
         gather_info<N, C::K, T>(beta, gtab, stg, out + f * NWK);
         sync();

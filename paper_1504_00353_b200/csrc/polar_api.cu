@@ -63,6 +63,7 @@ struct polar_code {
     int variant = 0;              // 0 auto, 1 throughput, 2 latency (polar_code_set_variant)
     uint16_t* d_pos = nullptr;    // K information positions, ascending (encoder / generator)
     uint32_t* d_gtab = nullptr;   // gather table: info mask words, then info-bit prefix per word
+    void* d_gscratch[4] = {nullptr, nullptr, nullptr, nullptr};  // per variant global stage scratch
     uint32_t* d_info_mask = nullptr;  // N/32 words (>= 1), bit set = information position
     // host-buffer path (lazily allocated, guarded by mu)
     std::mutex mu;
@@ -104,6 +105,10 @@ static polar_status init_device(polar_code* h) {
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ[i], k, (int)(vs[i]->threads * vs[i]->frames),
                                                                *vs[i]->smem));
         if (h->occ[i] < 1) return fail(POLAR_ERR_CUDA, "decoder kernel variant %d cannot be resident", i);
+        if (vs[i]->gscratch) {  // one slot per resident frame group of the persistent grid
+            const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * vs[i]->gscratch;
+            CUDA_TRY(cudaMalloc(&h->d_gscratch[i], bytes));
+        }
     }
     std::vector<uint16_t> pos;
     std::vector<uint32_t> im(std::max<uint32_t>(1, h->N / 32), 0);
@@ -169,6 +174,8 @@ extern "C" void polar_code_destroy(polar_code* h) {
         cudaFree(h->d_pos);
         cudaFree(h->d_info_mask);
         cudaFree(h->d_gtab);
+        for (int i = 0; i < 4; ++i)
+            if (h->d_gscratch[i]) cudaFree(h->d_gscratch[i]);
         for (int i = 0; i < 2; ++i) {
             if (h->d_stage_llr[i]) cudaFree(h->d_stage_llr[i]);
             if (h->d_stage_out[i]) cudaFree(h->d_stage_out[i]);
@@ -247,7 +254,8 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     const unsigned grid = (unsigned)std::min<int64_t>((n + v.frames - 1) / v.frames, resident);
     long long nn = (long long)n;
     const uint32_t* gtab = h->d_gtab;
-    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab};
+    void* gs = h->d_gscratch[vi];
+    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs};
     CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(v.threads * v.frames), args, smem, s));
     return POLAR_OK;
 }

@@ -7,13 +7,15 @@
 
 namespace polar {
 
-// One compiled kernel: __global__ (const void* llr, long long n, uint32_t* out, const uint32_t* gtab).
+// One compiled kernel: __global__ (const void* llr, long long n, uint32_t* out, const uint32_t* gtab,
+// void* gscratch).
 // Held through pointers to per-code constants so the table is constant-initialised.
 struct Variant {
     const void* const* kern;
     const unsigned* smem;  // dynamic shared memory per CTA
     uint32_t threads;      // threads per frame group
     uint32_t frames;       // frame groups (frames decoded concurrently) per CTA
+    uint32_t gscratch;     // bytes of global stage scratch per frame group (0: none)
 };
 
 struct RegistryEntry {
