@@ -432,7 +432,7 @@ PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
 template <class P, int T, int n, bool CLAMP, class TS>
 PD_INLINE void cF(const TS* __restrict__ src, typename P::st_t* __restrict__ dst) {
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
-#pragma unroll 2
+#pragma unroll 4
     for (int i = CE * gtid<T>(); i < H; i += CE * T) {
         Chunk<P, CE> a, b;
         if constexpr (sizeof(typename P::st_t) == 1) {
@@ -449,7 +449,7 @@ PD_INLINE void cF(const TS* __restrict__ src, typename P::st_t* __restrict__ dst
 template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, class TS>
 PD_INLINE void cG(const TS* __restrict__ src, typename P::st_t* __restrict__ dst, const uint32_t* beta) {
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
-#pragma unroll 2
+#pragma unroll 4
     for (int i = CE * gtid<T>(); i < H; i += CE * T) {
         Chunk<P, CE> a, b;
         if constexpr (sizeof(typename P::st_t) == 1) {
