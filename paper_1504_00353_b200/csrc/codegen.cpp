@@ -311,7 +311,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         std::ostringstream body, subs;
         CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, {}, {}, 0, &sh};
         int acc = 0, sacc = 0, gacc = 0;
-        const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 2 : sp.N + 1);
+        const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         for (int m = sp.N / 2; m >= W; m /= 2) {
             ce.stage_off[m] = acc;
             acc += m;
@@ -360,7 +360,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     auto a16 = [](int x) { return (x + 15) & ~15; };
     int g_elems = 0;
     if (cta_phase) {
-        const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 2 : sp.N + 1);
+        const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         for (int m = sp.N / 2; m >= W; m /= 2)
             if (m >= gs) g_elems += m;
     }

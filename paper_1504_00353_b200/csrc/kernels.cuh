@@ -57,7 +57,7 @@ struct FrameLayout {
 };
 
 // FPC frame groups of T threads per CTA (FPC > 1 only with T = 32).
-// GTOP: the largest stages (N/2 by default) live in global scratch (L2-resident), one slot per frame
+// GTOP: the largest stages (N/2 and N/4 by default) live in global scratch (L2-resident), one slot per frame
 // group of the persistent grid, so that more frames fit in shared memory per SM.
 template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP>
 __global__ void __launch_bounds__(T * FPC)
