@@ -221,7 +221,9 @@ struct CtaEmitter {
     SharedFns* sh = nullptr;
 
     // GTOP (template flag of decode): the largest stages live in per-frame global scratch.
+    // The stage of size W (the register subtrees' input) is kept as f32 in `wst`.
     std::string stage(int m) {
+        if (m == W) return "wst";
         if (goff.count(m)) return "(GTOP ? gst + " + std::to_string(goff.at(m)) + " : stages + " + std::to_string(stage_off.at(m)) + ")";
         return "(stages + (GTOP ? " + std::to_string(soff.at(m)) + " : " + std::to_string(stage_off.at(m)) + "))";
     }
@@ -302,17 +304,18 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
       << "    static constexpr int W = " << W << ";\n";
     if (!cta_phase) {
         o << "    static constexpr int STAGE_ELEMS = 0;\n    static constexpr int STAGE_ELEMS_SMEM = 0;\n"
-          << "    static constexpr int GSTAGE_ELEMS = 0;\n";
+          << "    static constexpr int GSTAGE_ELEMS = 0;\n    static constexpr int WST = 0;\n";
         emit_warp_sub(o, t, 0, "decode_root", &sh);
         o << "    template <class P, int T, bool GTOP, class ChanT, class SyncT>\n"
-          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, typename P::st_t*, uint32_t* beta, const SyncT&) {\n"
+          << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, typename P::st_t*, typename P::v_t*,\n"
+          << "                                 uint32_t* beta, const SyncT&) {\n"
           << "        if (gtid<T>() < 32) decode_root<P>(chan, beta);\n    }\n";
     } else {
         std::ostringstream body, subs;
         CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, {}, {}, 0, &sh};
         int acc = 0, sacc = 0, gacc = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
-        for (int m = sp.N / 2; m >= W; m /= 2) {
+        for (int m = sp.N / 2; m > W; m /= 2) {
             ce.stage_off[m] = acc;
             acc += m;
             if (m >= gs) {
@@ -326,11 +329,12 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         ce.cta(0, "chan");
         o << "    static constexpr int STAGE_ELEMS = " << acc << ";\n"
           << "    static constexpr int STAGE_ELEMS_SMEM = " << sacc << ";  // GTOP layout\n"
-          << "    static constexpr int GSTAGE_ELEMS = " << gacc << ";\n";
+          << "    static constexpr int GSTAGE_ELEMS = " << gacc << ";\n"
+          << "    static constexpr int WST = " << W << ";  // f32 stage feeding the register subtrees\n";
         o << subs.str();
         o << "    template <class P, int T, bool GTOP, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
-          << "                                 uint32_t* beta, const SyncT& sync) {\n"
+          << "                                 typename P::v_t* wst, uint32_t* beta, const SyncT& sync) {\n"
           << body.str() << "    }\n";
     }
     o << "};\n\n}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
@@ -361,12 +365,12 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     int g_elems = 0;
     if (cta_phase) {
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
-        for (int m = sp.N / 2; m >= W; m /= 2)
+        for (int m = sp.N / 2; m > W; m /= 2)
             if (m >= gs) g_elems += m;
     }
     auto fpc = [&](const char* prof, bool chan_smem) {
         const int s = std::string(prof) == "PF32" ? 4 : 1;
-        const int stages = a16(std::max(0, cta_phase ? sp.N - W - g_elems : 0) * s);
+        const int stages = a16(std::max(0, cta_phase ? sp.N - 2 * W - g_elems : 0) * s) + (cta_phase ? a16(W * 4) : 0);
         const int outw = a16((sp.K + 31) / 32 * 4);
         const int per = (chan_smem ? 2 * a16(sp.N * s) : 0) + stages + a16(std::max(1, sp.N / 32) * 4) +
                         (stages >= outw ? 0 : outw) + 16;

@@ -23,6 +23,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 namespace pd {
@@ -100,6 +101,7 @@ struct PI8 {
     // -128 -> -127 (C8); int -> float by the exponent trick (integer ALU + one FADD)
     static PD_INLINE v_t ld(int8_t x) { return __int_as_float(0x4B400000 + max((int)x, -127)) - 12582912.0f; }
     static PD_INLINE int8_t st(v_t x) { return (int8_t)__float2int_rn(x); }
+    static PD_INLINE v_t ld(float x) { return x; }  // the f32 subtree-input stage
     static PD_INLINE v_t f(v_t a, v_t b) { return PF32::f(a, b); }
     // saturating adder (max(-127) P:848): clamp(x) = copysign(min(|x|, 127), x)
     static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) { return fminxs(PF32::g(a, b, beta), 127.0f); }
@@ -168,6 +170,15 @@ struct Chunk<PI8, CE> {
         if constexpr (CE == 16) *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
         else if constexpr (CE == 8) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
         else *reinterpret_cast<uint32_t*>(p) = w[0];
+    }
+    // the f32 stage feeding the register subtrees
+    PD_INLINE void store(float* p) const {
+#pragma unroll
+        for (int q = 0; q < CE / 4; ++q) {
+            const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&h[2 * q]));
+            const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&h[2 * q + 1]));
+            *reinterpret_cast<float4*>(p + 4 * q) = make_float4(lo.x, lo.y, hi.x, hi.y);
+        }
     }
     // F: h = f(h, b)
     PD_INLINE void f(const Chunk& b) {
@@ -429,8 +440,8 @@ PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
 // stages of the node; beta is the node's first word of the natural bit array.
 
 // CLAMP: the source is the channel (int8 -128 -> -127, reading C8); stages never need it.
-template <class P, int T, int n, bool CLAMP, class TS>
-PD_INLINE void cF(const TS* __restrict__ src, typename P::st_t* __restrict__ dst) {
+template <class P, int T, int n, bool CLAMP, class TS, class TD>
+PD_INLINE void cF(const TS* __restrict__ src, TD* __restrict__ dst) {
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
 #pragma unroll 4
     for (int i = CE * gtid<T>(); i < H; i += CE * T) {
@@ -446,8 +457,8 @@ PD_INLINE void cF(const TS* __restrict__ src, typename P::st_t* __restrict__ dst
         a.store(dst + i);
     }
 }
-template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, class TS>
-PD_INLINE void cG(const TS* __restrict__ src, typename P::st_t* __restrict__ dst, const uint32_t* beta) {
+template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, class TS, class TD>
+PD_INLINE void cG(const TS* __restrict__ src, TD* __restrict__ dst, const uint32_t* beta) {
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
 #pragma unroll 4
     for (int i = CE * gtid<T>(); i < H; i += CE * T) {
@@ -464,8 +475,8 @@ PD_INLINE void cG(const TS* __restrict__ src, typename P::st_t* __restrict__ dst
         a.store(dst + i);
     }
 }
-template <class P, int T, int n, bool CLAMP, class TS>
-PD_INLINE void cG0R(const TS* __restrict__ src, typename P::st_t* __restrict__ dst) {
+template <class P, int T, int n, bool CLAMP, class TS, class TD>
+PD_INLINE void cG0R(const TS* __restrict__ src, TD* __restrict__ dst) {
     cG<P, T, n, CLAMP, true>(src, dst, nullptr);
 }
 template <class P, int T, int n, class TS>
@@ -478,8 +489,8 @@ PD_INLINE void cR1(const TS* __restrict__ src, uint32_t* beta) {
 // Repetition at CTA scope.  f32: pairwise-halving order (reading C13) run in
 // place on `scratch` (the free child stage of size n/2); int8: exact integer sum.  A lone
 // warp (T = 32, possibly one of several frame groups of a CTA) reduces with shuffles only.
-template <class P, int T, int n, class TS>
-PD_INLINE void cRep(const TS* __restrict__ src, typename P::st_t* scratch, uint32_t* beta) {
+template <class P, int T, int n, class TS, class TSc>
+PD_INLINE void cRep(const TS* __restrict__ src, TSc* scratch, uint32_t* beta) {
     using A = typename P::acc_t;
     bool decision;
     if constexpr (P::kExactSum) {

@@ -47,7 +47,9 @@ struct FrameLayout {
     // throughput warps double-buffer (prefetch the next frame), the latency CTA single-buffers
     static constexpr int NBUF = CHAN_SMEM ? (T == 32 ? 2 : 1) : 0;
     static constexpr int BUF = align16(FRAME_BYTES);
-    static constexpr int STAGES = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t));
+    static constexpr int STAGES = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t)) +
+                                  align16(C::WST * (int)sizeof(typename P::v_t));
+    static constexpr int WST_OFF = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t));
     static constexpr int BETA = align16((C::N >= 32 ? C::N / 32 : 1) * 4);
     // output staging words: the stage area is free after the decode when it is large enough
     static constexpr int OUTW = align16((C::K + 31) / 32 * 4);
@@ -77,6 +79,7 @@ __global__ void __launch_bounds__(T * FPC)
     in_t* const buf0 = (in_t*)smem;
     in_t* const buf1 = (in_t*)(smem + (DBL ? L::BUF : 0));
     st_t* const stages = (st_t*)(smem + L::NBUF * L::BUF);
+    typename P::v_t* const wst = (typename P::v_t*)(smem + L::NBUF * L::BUF + L::WST_OFF);
     uint32_t* const beta = (uint32_t*)(smem + L::NBUF * L::BUF + L::STAGES);
     uint32_t* const stg = (uint32_t*)(L::STG ? smem + L::NBUF * L::BUF + L::STAGES + L::BETA : (unsigned char*)stages);
     uint64_t* const bar = (uint64_t*)(smem + L::NBUF * L::BUF + L::STAGES + L::BETA + L::STG);
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(T * FPC)
             for (int k = tid; k < N / 32; k += T) beta[k] = 0;
             sync();
         }
-        C::template decode<P, T, GTOP>(chan, stages, gst, beta, sync);
+        C::template decode<P, T, GTOP>(chan, stages, gst, wst, beta, sync);
         sync();
         gather_info<N, C::K, T>(beta, gtab, stg, out + f * NWK);
         sync();
