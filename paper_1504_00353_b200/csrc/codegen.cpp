@@ -223,16 +223,35 @@ struct CtaEmitter {
     // GTOP (template flag of decode): the largest stages live in per-frame global scratch.
     // The stage of size W (the register subtrees' input) is kept as f32 in `wst`.
     std::string stage(int m) {
-        if (m == W) return "wst";
+        if (m == W) return "@W";  // f32 `wst` in the latency variant (WF32), else an int8/f32 stage
         if (goff.count(m)) return "(GTOP ? gst + " + std::to_string(goff.at(m)) + " : stages + " + std::to_string(stage_off.at(m)) + ")";
         return "(stages + (GTOP ? " + std::to_string(soff.at(m)) + " : " + std::to_string(stage_off.at(m)) + "))";
+    }
+
+    // Emit one statement; "@W" (the stage of size W) becomes `wst` under WF32, else its slot
+    // in the stage arrays.
+    void emit(const std::string& stmt) {
+        const size_t p = stmt.find("@W");
+        if (p == std::string::npos) {
+            body << "        " << stmt << "\n";
+            return;
+        }
+        auto subst = [&](const std::string& by) {
+            std::string r = stmt;
+            for (size_t q; (q = r.find("@W")) != std::string::npos;) r.replace(q, 2, by);
+            return r;
+        };
+        const std::string slot = soff.count(W) ? "(stages + (GTOP ? " + std::to_string(soff.at(W)) + " : " +
+                                                     std::to_string(stage_off.at(W)) + "))"
+                                               : "(stages + " + std::to_string(stage_off.at(W)) + ")";
+        body << "        if constexpr (WF32) { " << subst("wst") << " } else { " << subst(slot) << " }\n";
     }
 
     void sub_call(int id, const std::string& src) {
         std::string fname = "sub" + std::to_string(n_subs++);
         emit_warp_sub(subs, t, id, fname, sh);
-        body << "        if (gtid<T>() < 32) " << fname << "<P>(" << src << ", beta);\n"
-             << "        sync();\n";
+        emit("if (gtid<T>() < 32) " + fname + "<P>(" + src + ", beta);");
+        emit("sync();");
     }
 
     void child(int id, const std::string& src) {
@@ -252,14 +271,16 @@ struct CtaEmitter {
             case Kind::Rate0:
                 return;
             case Kind::Rate1:
-                body << "        cR1<P, T, " << N_ << ">(" << src << ", " << B << ");\n        sync();\n";
+                emit("cR1<P, T, " + N_ + ">(" + src + ", " + B + ");");
+                emit("sync();");
                 return;
             case Kind::Rep:
-                body << "        cRep<P, T, " << N_ << ">(" << src << ", " << stage(n / 2) << ", " << B
-                     << ");\n        sync();\n";
+                emit("cRep<P, T, " + N_ + ">(" + src + ", " + stage(n / 2) + ", " + B + ");");
+                emit("sync();");
                 return;
             case Kind::Spc:
-                body << "        cSPC<P, T, " << N_ << ">(" << src << ", " << B << ");\n        sync();\n";
+                emit("cSPC<P, T, " + N_ + ">(" + src + ", " + B + ");");
+                emit("sync();");
                 return;
             case Kind::Split:
                 break;
@@ -269,17 +290,24 @@ struct CtaEmitter {
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
         if (l.kind == Kind::Rate0) {
-            body << "        cG0R<P, T, " << N_ << ", " << CL << ">(" << src << ", " << D << ");\n        sync();\n";
+            emit("cG0R<P, T, " + N_ + ", " + CL + ">(" + src + ", " + D + ");");
+            emit("sync();");
+            if (id == 0) emit("sync.root_g_done();");
             child(v.right, D);
-            body << "        cComb0R<T, " << N_ << ">(" << B << ");\n        sync();\n";
+            emit("cComb0R<T, " + N_ + ">(" + B + ");");
+            emit("sync();");
             return;
         }
-        body << "        cF<P, T, " << N_ << ", " << CL << ">(" << src << ", " << D << ");\n        sync();\n";
+        emit("cF<P, T, " + N_ + ", " + CL + ">(" + src + ", " + D + ");");
+        emit("sync();");
         child(v.left, D);
         if (r.kind == Kind::Rate0) return;
-        body << "        cG<P, T, " << N_ << ", " << CL << ", false>(" << src << ", " << D << ", " << B << ");\n        sync();\n";
+        emit("cG<P, T, " + N_ + ", " + CL + ", false>(" + src + ", " + D + ", " + B + ");");
+        emit("sync();");
+        if (id == 0) emit("sync.root_g_done();");
         child(v.right, D);
-        body << "        cComb<T, " << N_ << ">(" << B << ");\n        sync();\n";
+        emit("cComb<T, " + N_ + ">(" + B + ");");
+        emit("sync();");
     }
 };
 
@@ -306,7 +334,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         o << "    static constexpr int STAGE_ELEMS = 0;\n    static constexpr int STAGE_ELEMS_SMEM = 0;\n"
           << "    static constexpr int GSTAGE_ELEMS = 0;\n    static constexpr int WST = 0;\n";
         emit_warp_sub(o, t, 0, "decode_root", &sh);
-        o << "    template <class P, int T, bool GTOP, class ChanT, class SyncT>\n"
+        o << "    template <class P, int T, bool GTOP, bool WF32, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, typename P::st_t*, typename P::v_t*,\n"
           << "                                 uint32_t* beta, const SyncT&) {\n"
           << "        if (gtid<T>() < 32) decode_root<P>(chan, beta);\n    }\n";
@@ -315,7 +343,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, {}, {}, 0, &sh};
         int acc = 0, sacc = 0, gacc = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
-        for (int m = sp.N / 2; m > W; m /= 2) {
+        for (int m = sp.N / 2; m >= W; m /= 2) {
             ce.stage_off[m] = acc;
             acc += m;
             if (m >= gs) {
@@ -332,7 +360,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
           << "    static constexpr int GSTAGE_ELEMS = " << gacc << ";\n"
           << "    static constexpr int WST = " << W << ";  // f32 stage feeding the register subtrees\n";
         o << subs.str();
-        o << "    template <class P, int T, bool GTOP, class ChanT, class SyncT>\n"
+        o << "    template <class P, int T, bool GTOP, bool WF32, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
           << "                                 typename P::v_t* wst, uint32_t* beta, const SyncT& sync) {\n"
           << body.str() << "    }\n";
@@ -365,12 +393,12 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     int g_elems = 0;
     if (cta_phase) {
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
-        for (int m = sp.N / 2; m > W; m /= 2)
+        for (int m = sp.N / 2; m >= W; m /= 2)
             if (m >= gs) g_elems += m;
     }
     auto fpc = [&](const char* prof, bool chan_smem) {
         const int s = std::string(prof) == "PF32" ? 4 : 1;
-        const int stages = a16(std::max(0, cta_phase ? sp.N - 2 * W - g_elems : 0) * s) + (cta_phase ? a16(W * 4) : 0);
+        const int stages = a16(std::max(0, cta_phase ? sp.N - W - g_elems : 0) * s);
         const int outw = a16((sp.K + 31) / 32 * 4);
         const int per = (chan_smem ? 2 * a16(sp.N * s) : 0) + stages + a16(std::max(1, sp.N / 32) * 4) +
                         (stages >= outw ? 0 : outw) + 16;

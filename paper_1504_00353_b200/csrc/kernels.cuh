@@ -29,12 +29,20 @@ PD_INLINE void prefetch_l2(const void* p, uint32_t bytes) {
 // Op-boundary barrier of a frame group.  Latency variant: the whole CTA.  Throughput variant:
 // all active warps of the CTA (named barrier 1), so that the FPC warps, each decoding its
 // own frame through the same unrolled code, stay in lockstep and share instruction fetch.
+// It also carries the L2 prefetch of the group's next frame, issued right after the root G
+// (the last read of the current frame's channel LLRs), so that each frame slot holds one
+// channel in L2 at a time.
 template <int T>
 struct OpSync {
     uint32_t threads;
+    const void* next;     // next frame's channel LLRs (nullptr: none / not prefetched)
+    uint32_t next_bytes;
     PD_INLINE void operator()() const {
         if constexpr (T > 32) __syncthreads();
         else asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
+    }
+    PD_INLINE void root_g_done() const {
+        if (next && (threadIdx.x & (T - 1)) == 0) prefetch_l2(next, next_bytes);
     }
 };
 
@@ -47,9 +55,11 @@ struct FrameLayout {
     // throughput warps double-buffer (prefetch the next frame), the latency CTA single-buffers
     static constexpr int NBUF = CHAN_SMEM ? (T == 32 ? 2 : 1) : 0;
     static constexpr int BUF = align16(FRAME_BYTES);
-    static constexpr int STAGES = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t)) +
-                                  align16(C::WST * (int)sizeof(typename P::v_t));
+    // WF32 (latency variant): the stage of size W, read element by element by the register
+    // subtrees, is kept as f32 in its own array
+    static constexpr bool WF32 = T > 32;
     static constexpr int WST_OFF = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t));
+    static constexpr int STAGES = WST_OFF + (WF32 ? align16(C::WST * (int)sizeof(typename P::v_t)) : 0);
     static constexpr int BETA = align16((C::N >= 32 ? C::N / 32 : 1) * 4);
     // output staging words: the stage area is free after the decode when it is large enough
     static constexpr int OUTW = align16((C::K + 31) / 32 * 4);
@@ -104,8 +114,11 @@ __global__ void __launch_bounds__(T * FPC)
     for (int it = 0; f < n_frames; f += stride, ++it) {
         // warps of this round that have a frame: they alone take part in the op barriers
         const long long base = f - grp;
-        const OpSync<T> sync{(uint32_t)(32 * (FPC > 1 ? (int)min((long long)FPC, n_frames - base) : 1))};
         const long long nf = f + stride;
+        // without shared-memory ingest the next frame is prefetched into L2 after the root G
+        const bool pf = !CHAN_SMEM && L::kBulk && C::STAGE_ELEMS > 0 && nf < n_frames;
+        const OpSync<T> sync{(uint32_t)(32 * (FPC > 1 ? (int)min((long long)FPC, n_frames - base) : 1)),
+                             pf ? (const void*)(llr + nf * N) : nullptr, (uint32_t)L::FRAME_BYTES};
         const in_t* chan;
         if constexpr (TMA) {
             in_t* cur = (DBL && (it & 1)) ? buf1 : buf0;
@@ -121,14 +134,14 @@ __global__ void __launch_bounds__(T * FPC)
             sync();
             chan = buf0;
         } else {
-            if (L::kBulk && leader && nf < n_frames) prefetch_l2(llr + nf * N, L::FRAME_BYTES);
+            if (C::STAGE_ELEMS == 0 && L::kBulk && leader && nf < n_frames) prefetch_l2(llr + nf * N, L::FRAME_BYTES);
             chan = llr + f * N;
         }
         if constexpr (C::STAGE_ELEMS > 0) {
             for (int k = tid; k < N / 32; k += T) beta[k] = 0;
             sync();
         }
-        C::template decode<P, T, GTOP>(chan, stages, gst, wst, beta, sync);
+        C::template decode<P, T, GTOP, L::WF32>(chan, stages, gst, wst, beta, sync);
         sync();
         gather_info<N, C::K, T>(beta, gtab, stg, out + f * NWK);
         sync();
