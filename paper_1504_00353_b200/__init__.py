@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpolar.so")
+# POLAR_LIB selects an experiment build (tools/variant_build.sh); default: the in-tree library.
+LIB_PATH = os.environ.get("POLAR_LIB", os.path.join(_HERE, "libpolar.so"))
 
 POLAR_OK = 0
 POLAR_ERR_INVALID_ARGUMENT = 1

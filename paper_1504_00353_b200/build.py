@@ -18,16 +18,19 @@ from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "build")
+# Experiment builds (tools/variant_build.sh) redirect these; the product build uses the defaults.
+BUILD = os.environ.get("POLAR_BUILD_DIR", os.path.join(PKG, "build"))
 GEN = os.path.join(BUILD, "gen")
 OBJ = os.path.join(BUILD, "obj")
-LIB = os.path.join(PKG, "libpolar.so")
+LIB = os.environ.get("POLAR_LIB_OUT", os.path.join(PKG, "libpolar.so"))
+SPEC_FILES = os.environ.get("POLAR_CODES", "codes.txt,codes_random.txt").split(",")
+EXTRA = os.environ.get("POLAR_NVCC_EXTRA", "").split()
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", CSRC, "-I", INCLUDE,
-                  "-Xptxas", "-v", "--resource-usage"]
+                  "-Xptxas", "-v", "--resource-usage"] + EXTRA
 HEADERS = ["decoder.cuh", "kernels.cuh", "registry.hpp", "tree.hpp"]
 
 
@@ -76,8 +79,8 @@ def build(verbose: bool = True, jobs: int | None = None) -> str:
     # 2. emit into a scratch dir, then replace only the files whose content changed
     spec = os.path.join(BUILD, "codes_all.txt")
     with open(spec, "w") as f:
-        for name in ("codes.txt", "codes_random.txt"):
-            p = os.path.join(PKG, name)
+        for name in SPEC_FILES:
+            p = name if os.path.isabs(name) else os.path.join(PKG, name)
             if os.path.exists(p):
                 f.write(open(p).read() + "\n")
     scratch = GEN + ".new"

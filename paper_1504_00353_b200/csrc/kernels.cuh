@@ -116,7 +116,11 @@ __global__ void __launch_bounds__(T * FPC)
         const long long base = f - grp;
         const long long nf = f + stride;
         // without shared-memory ingest the next frame is prefetched into L2 after the root G
+#ifdef POLAR_NO_PREFETCH
+        const bool pf = false;
+#else
         const bool pf = !CHAN_SMEM && L::kBulk && C::STAGE_ELEMS > 0 && nf < n_frames;
+#endif
         const OpSync<T> sync{(uint32_t)(32 * (FPC > 1 ? (int)min((long long)FPC, n_frames - base) : 1)),
                              pf ? (const void*)(llr + nf * N) : nullptr, (uint32_t)L::FRAME_BYTES};
         const in_t* chan;

@@ -1,0 +1,7 @@
+#!/bin/bash
+# Bench each experiment variant (variants/<name>/libpolar.so) on the headline workload.
+mkdir -p gpurun_out
+for v in "$@"; do
+  POLAR_LIB=variants/$v/libpolar.so timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-extra > gpurun_out/var_$v.json 2> gpurun_out/var_$v.err
+  python -c "import json,sys; d=json.load(open('gpurun_out/var_$v.json')); print('$v', round(d['value'],1), 'Gbps', round(d['ms_per_step'],3), 'ms')" || tail -3 gpurun_out/var_$v.err
+done
