@@ -116,10 +116,12 @@ __global__ void __launch_bounds__(T * FPC)
         const long long base = f - grp;
         const long long nf = f + stride;
         // without shared-memory ingest the next frame is prefetched into L2 after the root G
-#ifdef POLAR_NO_PREFETCH
-        const bool pf = false;
-#else
+        // Off by default: measured slower at N = 32768 (each frame slot would then hold a second
+        // channel in L2 besides its live stage scratch; profiles/r1_sweep.md).
+#ifdef POLAR_PREFETCH_NEXT
         const bool pf = !CHAN_SMEM && L::kBulk && C::STAGE_ELEMS > 0 && nf < n_frames;
+#else
+        const bool pf = false;
 #endif
         const OpSync<T> sync{(uint32_t)(32 * (FPC > 1 ? (int)min((long long)FPC, n_frames - base) : 1)),
                              pf ? (const void*)(llr + nf * N) : nullptr, (uint32_t)L::FRAME_BYTES};
