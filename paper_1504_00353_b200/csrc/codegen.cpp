@@ -254,6 +254,13 @@ struct CtaEmitter {
         emit("sync();");
     }
 
+    // State space (SP_GLOBAL 0 / SP_SHARED 1) of a stage, as a C++ constant expression.
+    std::string space(int m) {
+        if (m == W) return "1";
+        if (goff.count(m)) return "(GTOP ? 0 : 1)";
+        return "1";
+    }
+
     void child(int id, const std::string& src) {
         const Node& v = t.nodes[id];
         if (v.kind == Kind::Rate0) return;  // beta zeroed at frame start
@@ -262,6 +269,7 @@ struct CtaEmitter {
     }
 
     void cta(int id, const std::string& src) {
+        const std::string SS = src == "chan" ? "CHS" : space(t.nodes[id].n);
         const Node& v = t.nodes[id];
         const int n = v.n;
         const std::string N_ = std::to_string(n);
@@ -290,7 +298,7 @@ struct CtaEmitter {
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
         if (l.kind == Kind::Rate0) {
-            emit("cG0R<P, T, " + N_ + ", " + CL + ">(" + src + ", " + D + ");");
+            emit("cG0R<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ">(" + src + ", " + D + ");");
             emit("sync();");
             if (id == 0) emit("sync.root_g_done();");
             child(v.right, D);
@@ -298,11 +306,11 @@ struct CtaEmitter {
             emit("sync();");
             return;
         }
-        emit("cF<P, T, " + N_ + ", " + CL + ">(" + src + ", " + D + ");");
+        emit("cF<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ">(" + src + ", " + D + ");");
         emit("sync();");
         child(v.left, D);
         if (r.kind == Kind::Rate0) return;
-        emit("cG<P, T, " + N_ + ", " + CL + ", false>(" + src + ", " + D + ", " + B + ");");
+        emit("cG<P, T, " + N_ + ", " + CL + ", false, " + SS + ", " + space(h) + ">(" + src + ", " + D + ", " + B + ");");
         emit("sync();");
         if (id == 0) emit("sync.root_g_done();");
         child(v.right, D);
@@ -334,7 +342,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         o << "    static constexpr int STAGE_ELEMS = 0;\n    static constexpr int STAGE_ELEMS_SMEM = 0;\n"
           << "    static constexpr int GSTAGE_ELEMS = 0;\n    static constexpr int WST = 0;\n";
         emit_warp_sub(o, t, 0, "decode_root", &sh);
-        o << "    template <class P, int T, bool GTOP, bool WF32, class ChanT, class SyncT>\n"
+        o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, typename P::st_t*, typename P::v_t*,\n"
           << "                                 uint32_t* beta, const SyncT&) {\n"
           << "        if (gtid<T>() < 32) decode_root<P>(chan, beta);\n    }\n";
@@ -360,7 +368,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
           << "    static constexpr int GSTAGE_ELEMS = " << gacc << ";\n"
           << "    static constexpr int WST = " << W << ";  // f32 stage feeding the register subtrees\n";
         o << subs.str();
-        o << "    template <class P, int T, bool GTOP, bool WF32, class ChanT, class SyncT>\n"
+        o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
           << "                                 typename P::v_t* wst, uint32_t* beta, const SyncT& sync) {\n"
           << body.str() << "    }\n";

@@ -23,6 +23,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -116,6 +117,49 @@ struct PI8 {
 // ------------------------------------------------------------- vector chunks (CTA scope)
 // CTA-scope ops move CE consecutive elements per thread: float4 (f32) or 4/8/16 packed int8.
 
+// Vector loads/stores with an explicit state space (SP_SHARED / SP_GLOBAL), so that the
+// stage ops can be shared non-inlined functions without falling back to generic accesses.
+enum : int { SP_GLOBAL = 0, SP_SHARED = 1 };
+
+template <int SP, int BYTES>
+PD_INLINE void vld(const void* p, uint32_t* w) {
+    if constexpr (SP == SP_SHARED) {
+        const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+        if constexpr (BYTES == 16)
+            asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(a));
+        else if constexpr (BYTES == 8)
+            asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(a));
+        else
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[0]) : "r"(a));
+    } else {
+        if constexpr (BYTES == 16)
+            asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p));
+        else if constexpr (BYTES == 8)
+            asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "l"(p));
+        else
+            asm volatile("ld.global.u32 %0, [%1];" : "=r"(w[0]) : "l"(p));
+    }
+}
+template <int SP, int BYTES>
+PD_INLINE void vst(void* p, const uint32_t* w) {
+    if constexpr (SP == SP_SHARED) {
+        const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
+        if constexpr (BYTES == 16)
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]) : "memory");
+        else if constexpr (BYTES == 8)
+            asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(w[0]), "r"(w[1]) : "memory");
+        else
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(w[0]) : "memory");
+    } else {
+        if constexpr (BYTES == 16)
+            asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]) : "memory");
+        else if constexpr (BYTES == 8)
+            asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(w[0]), "r"(w[1]) : "memory");
+        else
+            asm volatile("st.global.u32 [%0], %1;" ::"l"(p), "r"(w[0]) : "memory");
+    }
+}
+
 template <class P, int CE>
 struct Chunk;
 
@@ -123,11 +167,18 @@ template <int CE>
 struct Chunk<PF32, CE> {
     static_assert(CE == 4, "");
     float v[4];
-    PD_INLINE void load(const float* p) {
-        const float4 x = *reinterpret_cast<const float4*>(p);
-        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    template <int SP>
+    PD_INLINE void load(const void* p, bool = false) {
+        uint32_t w[4];
+        vld<SP, 16>(p, w);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __uint_as_float(w[k]);
     }
-    PD_INLINE void store(float* p) const { *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]); }
+    template <int SP, bool F32OUT>
+    PD_INLINE void store(void* p) const {
+        const uint32_t w[4] = {__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])};
+        vst<SP, 16>(p, w);
+    }
 };
 
 // int8 stages are processed as integer-valued f16x2 (exact: |values| <= 254 before the clamp).
@@ -149,35 +200,30 @@ struct Chunk<PI8, CE> {
             }
         }
     }
-    PD_INLINE void load(const int8_t* p, bool clamp = false) {
+    template <int SP>
+    PD_INLINE void load(const void* p, bool clamp = false) {
         uint32_t w[CE / 4];
-        if constexpr (CE == 16) {
-            const uint4 x = *reinterpret_cast<const uint4*>(p);
-            w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
-        } else if constexpr (CE == 8) {
-            const uint2 x = *reinterpret_cast<const uint2*>(p);
-            w[0] = x.x; w[1] = x.y;
-        } else {
-            w[0] = *reinterpret_cast<const uint32_t*>(p);
-        }
+        vld<SP, CE>(p, w);
         unpack(w, clamp);
     }
-    PD_INLINE void store(int8_t* p) const {
-        uint32_t w[CE / 4];
+    // F32OUT: the f32 stage feeding the register subtrees (latency variant), else int8
+    template <int SP, bool F32OUT>
+    PD_INLINE void store(void* p) const {
+        if constexpr (F32OUT) {
 #pragma unroll
-        for (int q = 0; q < CE / 4; ++q)
-            w[q] = __byte_perm(h2add(h[2 * q], 0x64806480u), h2add(h[2 * q + 1], 0x64806480u), 0x6420) ^ 0x80808080u;
-        if constexpr (CE == 16) *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
-        else if constexpr (CE == 8) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
-        else *reinterpret_cast<uint32_t*>(p) = w[0];
-    }
-    // the f32 stage feeding the register subtrees
-    PD_INLINE void store(float* p) const {
+            for (int q = 0; q < CE / 4; ++q) {
+                const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&h[2 * q]));
+                const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&h[2 * q + 1]));
+                const uint32_t w[4] = {__float_as_uint(lo.x), __float_as_uint(lo.y), __float_as_uint(hi.x),
+                                       __float_as_uint(hi.y)};
+                vst<SP, 16>((float*)p + 4 * q, w);
+            }
+        } else {
+            uint32_t w[CE / 4];
 #pragma unroll
-        for (int q = 0; q < CE / 4; ++q) {
-            const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&h[2 * q]));
-            const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&h[2 * q + 1]));
-            *reinterpret_cast<float4*>(p + 4 * q) = make_float4(lo.x, lo.y, hi.x, hi.y);
+            for (int q = 0; q < CE / 4; ++q)
+                w[q] = __byte_perm(h2add(h[2 * q], 0x64806480u), h2add(h[2 * q + 1], 0x64806480u), 0x6420) ^ 0x80808080u;
+            vst<SP, CE>(p, w);
         }
     }
     // F: h = f(h, b)
@@ -440,44 +486,50 @@ PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
 // stages of the node; beta is the node's first word of the natural bit array.
 
 // CLAMP: the source is the channel (int8 -128 -> -127, reading C8); stages never need it.
-template <class P, int T, int n, bool CLAMP, class TS, class TD>
-PD_INLINE void cF(const TS* __restrict__ src, TD* __restrict__ dst) {
+// SS / DS: state spaces of source and destination.  F32OUT: int8 profile writing the f32
+// subtree-input stage.  Every distinct instance is one non-inlined function shared by all
+// call sites of the unrolled decoder (the stage ops are loops; inlining ~100 of them made
+// the N = 32768 kernels ~40% larger, profiles/r1_history.md).
+template <class P, int T, int n, bool CLAMP, int SS, int DS, bool F32OUT>
+__device__ __noinline__ void cF_impl(const void* src, void* dst) {
+    using S = typename P::st_t;
+    using D = typename std::conditional<F32OUT, float, S>::type;
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
 #pragma unroll 4
     for (int i = CE * gtid<T>(); i < H; i += CE * T) {
         Chunk<P, CE> a, b;
-        if constexpr (sizeof(typename P::st_t) == 1) {
-            a.load(src + i, CLAMP);
-            b.load(src + i + H, CLAMP);
-        } else {
-            a.load(src + i);
-            b.load(src + i + H);
-        }
+        a.template load<SS>((const S*)src + i, CLAMP);
+        b.template load<SS>((const S*)src + i + H, CLAMP);
         chunk_f(a, b);
-        a.store(dst + i);
+        a.template store<DS, F32OUT>((D*)dst + i);
     }
 }
-template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, class TS, class TD>
-PD_INLINE void cG(const TS* __restrict__ src, TD* __restrict__ dst, const uint32_t* beta) {
+template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, bool F32OUT>
+__device__ __noinline__ void cG_impl(const void* src, void* dst, const uint32_t* beta) {
+    using S = typename P::st_t;
+    using D = typename std::conditional<F32OUT, float, S>::type;
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
 #pragma unroll 4
     for (int i = CE * gtid<T>(); i < H; i += CE * T) {
         Chunk<P, CE> a, b;
-        if constexpr (sizeof(typename P::st_t) == 1) {
-            a.load(src + i, CLAMP);
-            b.load(src + i + H, CLAMP);
-        } else {
-            a.load(src + i);
-            b.load(src + i + H);
-        }
+        a.template load<SS>((const S*)src + i, CLAMP);
+        b.template load<SS>((const S*)src + i + H, CLAMP);
         if constexpr (ZERO_LEFT) chunk_g0(a, b);
         else chunk_g(a, b, beta[i >> 5] >> (i & 31));
-        a.store(dst + i);
+        a.template store<DS, F32OUT>((D*)dst + i);
     }
 }
-template <class P, int T, int n, bool CLAMP, class TS, class TD>
-PD_INLINE void cG0R(const TS* __restrict__ src, TD* __restrict__ dst) {
-    cG<P, T, n, CLAMP, true>(src, dst, nullptr);
+template <class P, int T, int n, bool CLAMP, int SS, int DS, class TS, class TD>
+PD_INLINE void cF(const TS* src, TD* dst) {
+    cF_impl<P, T, n, CLAMP, SS, DS, sizeof(TD) == 4 && sizeof(typename P::st_t) == 1>(src, dst);
+}
+template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, class TS, class TD>
+PD_INLINE void cG(const TS* src, TD* dst, const uint32_t* beta) {
+    cG_impl<P, T, n, CLAMP, ZERO_LEFT, SS, DS, sizeof(TD) == 4 && sizeof(typename P::st_t) == 1>(src, dst, beta);
+}
+template <class P, int T, int n, bool CLAMP, int SS, int DS, class TS, class TD>
+PD_INLINE void cG0R(const TS* src, TD* dst) {
+    cG_impl<P, T, n, CLAMP, true, SS, DS, sizeof(TD) == 4 && sizeof(typename P::st_t) == 1>(src, dst, nullptr);
 }
 template <class P, int T, int n, class TS>
 PD_INLINE void cR1(const TS* __restrict__ src, uint32_t* beta) {

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(T * FPC)
             for (int k = tid; k < N / 32; k += T) beta[k] = 0;
             sync();
         }
-        C::template decode<P, T, GTOP, L::WF32>(chan, stages, gst, wst, beta, sync);
+        C::template decode<P, T, GTOP, L::WF32, CHAN_SMEM ? SP_SHARED : SP_GLOBAL>(chan, stages, gst, wst, beta, sync);
         sync();
         gather_info<N, C::K, T>(beta, gtab, stg, out + f * NWK);
         sync();
