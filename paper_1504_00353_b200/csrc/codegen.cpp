@@ -298,7 +298,7 @@ struct CtaEmitter {
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
         if (l.kind == Kind::Rate0) {
-            emit("cG0R<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ">(" + src + ", " + D + ");");
+            emit("cG0R<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
             emit("sync();");
             if (id == 0) emit("sync.root_g_done();");
             child(v.right, D);
@@ -306,11 +306,11 @@ struct CtaEmitter {
             emit("sync();");
             return;
         }
-        emit("cF<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ">(" + src + ", " + D + ");");
+        emit("cF<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
         emit("sync();");
         child(v.left, D);
         if (r.kind == Kind::Rate0) return;
-        emit("cG<P, T, " + N_ + ", " + CL + ", false, " + SS + ", " + space(h) + ">(" + src + ", " + D + ", " + B + ");");
+        emit("cG<P, T, " + N_ + ", " + CL + ", false, " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ", " + B + ");");
         emit("sync();");
         if (id == 0) emit("sync.root_g_done();");
         child(v.right, D);
@@ -371,6 +371,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
           << "                                 typename P::v_t* wst, uint32_t* beta, const SyncT& sync) {\n"
+          << "        constexpr bool NI = T == 32 && N >= 8192;  // shared non-inlined stage ops\n"
           << body.str() << "    }\n";
     }
     o << "};\n\n}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";

@@ -491,7 +491,7 @@ PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
 // call sites of the unrolled decoder (the stage ops are loops; inlining ~100 of them made
 // the N = 32768 kernels ~40% larger, profiles/r1_history.md).
 template <class P, int T, int n, bool CLAMP, int SS, int DS, bool F32OUT>
-__device__ __noinline__ void cF_impl(const void* src, void* dst) {
+PD_INLINE void cF_body(const void* src, void* dst) {
     using S = typename P::st_t;
     using D = typename std::conditional<F32OUT, float, S>::type;
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
@@ -505,7 +505,7 @@ __device__ __noinline__ void cF_impl(const void* src, void* dst) {
     }
 }
 template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, bool F32OUT>
-__device__ __noinline__ void cG_impl(const void* src, void* dst, const uint32_t* beta) {
+PD_INLINE void cG_body(const void* src, void* dst, const uint32_t* beta) {
     using S = typename P::st_t;
     using D = typename std::conditional<F32OUT, float, S>::type;
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
@@ -519,17 +519,31 @@ __device__ __noinline__ void cG_impl(const void* src, void* dst, const uint32_t*
         a.template store<DS, F32OUT>((D*)dst + i);
     }
 }
-template <class P, int T, int n, bool CLAMP, int SS, int DS, class TS, class TD>
+template <class P, int T, int n, bool CLAMP, int SS, int DS, bool F32OUT>
+__device__ __noinline__ void cF_impl(const void* src, void* dst) {
+    cF_body<P, T, n, CLAMP, SS, DS, F32OUT>(src, dst);
+}
+template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, bool F32OUT>
+__device__ __noinline__ void cG_impl(const void* src, void* dst, const uint32_t* beta) {
+    cG_body<P, T, n, CLAMP, ZERO_LEFT, SS, DS, F32OUT>(src, dst, beta);
+}
+// NI: call the shared non-inlined instance (throughput variant of large codes); otherwise
+// inline (the call costs latency on the batch-1 critical path).
+template <class P, int T, int n, bool CLAMP, int SS, int DS, bool NI, class TS, class TD>
 PD_INLINE void cF(const TS* src, TD* dst) {
-    cF_impl<P, T, n, CLAMP, SS, DS, sizeof(TD) == 4 && sizeof(typename P::st_t) == 1>(src, dst);
+    constexpr bool F32OUT = sizeof(TD) == 4 && sizeof(typename P::st_t) == 1;
+    if constexpr (NI) cF_impl<P, T, n, CLAMP, SS, DS, F32OUT>(src, dst);
+    else cF_body<P, T, n, CLAMP, SS, DS, F32OUT>(src, dst);
 }
-template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, class TS, class TD>
+template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, bool NI, class TS, class TD>
 PD_INLINE void cG(const TS* src, TD* dst, const uint32_t* beta) {
-    cG_impl<P, T, n, CLAMP, ZERO_LEFT, SS, DS, sizeof(TD) == 4 && sizeof(typename P::st_t) == 1>(src, dst, beta);
+    constexpr bool F32OUT = sizeof(TD) == 4 && sizeof(typename P::st_t) == 1;
+    if constexpr (NI) cG_impl<P, T, n, CLAMP, ZERO_LEFT, SS, DS, F32OUT>(src, dst, beta);
+    else cG_body<P, T, n, CLAMP, ZERO_LEFT, SS, DS, F32OUT>(src, dst, beta);
 }
-template <class P, int T, int n, bool CLAMP, int SS, int DS, class TS, class TD>
+template <class P, int T, int n, bool CLAMP, int SS, int DS, bool NI, class TS, class TD>
 PD_INLINE void cG0R(const TS* src, TD* dst) {
-    cG_impl<P, T, n, CLAMP, true, SS, DS, sizeof(TD) == 4 && sizeof(typename P::st_t) == 1>(src, dst, nullptr);
+    cG<P, T, n, CLAMP, true, SS, DS, NI>(src, dst, nullptr);
 }
 template <class P, int T, int n, class TS>
 PD_INLINE void cR1(const TS* __restrict__ src, uint32_t* beta) {
