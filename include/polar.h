@@ -157,6 +157,11 @@ polar_status polar_count_errors(const polar_code* h, const uint32_t* decoded,
                                 const uint32_t* truth, int64_t n_frames, int64_t* counters,
                                 polar_stream stream);
 
+/* Diagnostics of POLAR_TRACE builds only (otherwise POLAR_ERR_UNSUPPORTED_CODE): copy the
+ * clock64() stamps the latency variant recorded after each operation of its last decoded
+ * frame 0 (host buffer, n entries; labels in build/gen/trace_<code>.txt). */
+polar_status polar_trace_fetch(const polar_code* h, uint64_t* host, uint32_t n);
+
 /* Number of specialised codes compiled into this library, and the i-th one's (N, K) and
  * frozen mask (host buffer of at least N bytes; may be NULL to query N and K only). */
 uint32_t polar_registry_size(void);

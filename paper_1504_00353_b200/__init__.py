@@ -28,7 +28,7 @@ EXPORTS = [
     "polar_code_query", "polar_code_schedule", "polar_code_mask", "polar_code_set_variant", "polar_decode_f32",
     "polar_decode_i8", "polar_decode_f32_host", "polar_decode_i8_host", "polar_construct_ga",
     "polar_encode_systematic", "polar_gen_bpsk_awgn", "polar_count_errors",
-    "polar_registry_size", "polar_registry_entry",
+    "polar_registry_size", "polar_registry_entry", "polar_trace_fetch",
 ]
 
 
@@ -69,6 +69,7 @@ def lib() -> C.CDLL:
                                           vp, vp, vp, vp]),
         "polar_count_errors": (C.c_int, [vp, vp, vp, C.c_int64, vp, vp]),
         "polar_registry_size": (C.c_uint32, []),
+        "polar_trace_fetch": (C.c_int, [vp, vp, C.c_uint32]),
         "polar_registry_entry": (C.c_int, [C.c_uint32, u32p, u32p, vp]),
     }
     for name, (res, args) in sig.items():
@@ -210,6 +211,12 @@ class PolarCode:
                       llr_f32=None, llr_i8=None, info=None, stream=None):
         _check(lib().polar_gen_bpsk_awgn(self._h, seed, first_frame, n, float(ebn0_db), float(q_scale),
                                          _ptr(llr_f32), _ptr(llr_i8), _ptr(info), _stream(stream)))
+
+    def trace(self, n: int) -> np.ndarray:
+        """clock64 stamps of the latency variant's last frame (POLAR_TRACE builds only)."""
+        out = np.zeros(n, np.uint64)
+        _check(lib().polar_trace_fetch(self._h, out.ctypes.data, n))
+        return out
 
     def count_errors(self, decoded, truth, counters, stream=None):
         n = decoded.shape[0]

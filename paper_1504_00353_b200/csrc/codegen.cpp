@@ -51,6 +51,17 @@ struct Spec {
 // Distinct small-subtree patterns emitted once as __noinline__ device functions, so that the
 // unrolled code of a large code stays small enough for the instruction caches: at (32768,29492)
 // the 120 size-32 split subtrees have 28 distinct frozen patterns.
+// Trace marks (POLAR_TRACE builds): PTRACE(k) records clock64() after op k of the latency
+// variant's critical path; labels[k] names it (written to gen/trace_<code>.txt).
+struct TraceMarks {
+    std::vector<std::string> labels;
+    std::string mark(const std::string& label) {
+        labels.push_back(label);
+        return "PTRACE(" + std::to_string(labels.size() - 1) + ");";
+    }
+};
+TraceMarks* g_marks = nullptr;
+
 struct SharedFns {
     const std::vector<uint8_t>& mask;
     std::set<int> sizes;                 // node sizes that are deduplicated
@@ -62,11 +73,15 @@ struct Emitter {
     const Tree& t;
     std::ostringstream& o;
     SharedFns* sh = nullptr;
+    bool marks = true;  // emit PTRACE marks (not inside shared noinline functions)
     int next_mask = 0;
     std::string ind = "        ";
     int body_root = -1;  // the node whose shared function body is being emitted
 
     std::string mask_name() { return "m" + std::to_string(next_mask++); }
+    void mk(const std::string& label) {
+        if (marks && g_marks) o << ind << g_marks->mark(label) << "\n";
+    }
 
     // Emit the warp-scope decode of node id (size n) at bit offset off relative to the
     // subtree root.  src: the C++ expression of its LLR source.  Returns the name of the
@@ -84,6 +99,7 @@ struct Emitter {
             for (int j = 0; j < (n >= 32 ? n / 32 : 1); ++j) args += (j ? ", " : "") + src_arr + "[" + std::to_string(j) + "]";
             const std::string m = mask_name();
             o << ind << "const uint32_t " << m << " = " << fn << "<P>(" << args << ");\n";
+            mk("shared<" + N_ + ">");
             if (n <= 32) return m;
             o << ind << "bw |= (uint64_t)" << m << " << " << s0 << ";\n";
             return "";
@@ -95,25 +111,31 @@ struct Emitter {
                 if (n <= 32) {
                     std::string m = mask_name();
                     o << ind << "const uint32_t " << m << " = wR1m<P, " << N_ << ">(" << src << ");\n";
+                    mk("Info<" + N_ + ">");
                     return m;
                 }
                 o << ind << "wR1<P, " << N_ << ", " << S0 << ">(" << src << ", bw);\n";
+                mk("Info<" + N_ + ">");
                 return "";
             case Kind::Rep:
                 if (n <= 32) {
                     std::string m = mask_name();
                     o << ind << "const uint32_t " << m << " = wRepm<P, " << N_ << ">(" << src << ");\n";
+                    mk("Repetition<" + N_ + ">");
                     return m;
                 }
                 o << ind << "wRep<P, " << N_ << ", " << S0 << ">(" << src << ", bw);\n";
+                mk("Repetition<" + N_ + ">");
                 return "";
             case Kind::Spc:
                 if (n <= 32) {
                     std::string m = mask_name();
                     o << ind << "const uint32_t " << m << " = wSPCm<P, " << N_ << ">(" << src << ");\n";
+                    mk("SPC<" + N_ + ">");
                     return m;
                 }
                 o << ind << "wSPC<P, " << N_ << ", " << S0 << ">(" << src << ", bw);\n";
+                mk("SPC<" + N_ + ">");
                 return "";
             case Kind::Split:
                 break;
@@ -127,6 +149,7 @@ struct Emitter {
         const Node& r = t.nodes[v.right];
         if (l.kind == Kind::Rate0) {
             o << ind << "wG0R<P, " << N_ << ">(" << src << ", " << child << ");\n";
+            mk("G_0R<" + N_ + ">");
             std::string mr = warp(v.right, off + h, csrc, child);
             if (n <= 32) {
                 std::string m = mask_name();
@@ -138,11 +161,13 @@ struct Emitter {
             return "";
         }
         o << ind << "wF<P, " << N_ << ">(" << src << ", " << child << ");\n";
+        mk("F<" + N_ + ">");
         std::string ml = warp(v.left, off, csrc, child);
         if (h == 32 && ml != "0u") o << ind << "wDeposit<" << s0 << ">(bw, " << ml << ");\n";
         if (r.kind == Kind::Rate0) return n <= 32 ? ml : "";
         o << ind << "wG<P, " << N_ << ", " << S0 << ">(" << src << ", " << child << ", bw, "
           << (n <= 32 ? ml : std::string("0u")) << ");\n";
+        mk("G<" + N_ + ">");
         std::string mr = warp(v.right, off + h, csrc, child);
         if (n <= 32) {
             std::string m = mask_name();
@@ -170,6 +195,7 @@ std::string Emitter::shared_fn(int id) {
     std::ostringstream body;
     Emitter e{t, body, sh};
     e.body_root = id;
+    e.marks = false;
     const int S = n >= 32 ? n / 32 : 1;
     for (int k = ilog2(n) - 1; k >= 0; --k)
         body << "    V r" << k << "[" << ((1 << k) >= 32 ? (1 << k) / 32 : 1) << "];\n";
@@ -230,7 +256,18 @@ struct CtaEmitter {
 
     // Emit one statement; "@W" (the stage of size W) becomes `wst` under WF32, else its slot
     // in the stage arrays.
+    std::string last_op;
     void emit(const std::string& stmt) {
+        if (stmt == "sync();" && g_marks) {
+            emit_raw(stmt);
+            std::string lab = last_op.rfind("if (gtid", 0) == 0 ? std::string("subtree") : last_op.substr(0, last_op.find('('));
+            emit_raw(g_marks->mark("cta:" + lab));
+            return;
+        }
+        if (stmt.rfind("sync.", 0) != 0) last_op = stmt;
+        emit_raw(stmt);
+    }
+    void emit_raw(const std::string& stmt) {
         const size_t p = stmt.find("@W");
         if (p == std::string::npos) {
             body << "        " << stmt << "\n";
@@ -333,6 +370,9 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     const bool cta_phase = sp.N > W;
     const int t_lat = cta_phase ? sp.T : 32;
     SharedFns sh{sp.mask, sp.dedup, {}, {}};
+    TraceMarks marks;
+    g_marks = &marks;
+    marks.mark("start");
     std::ostringstream o;
     o << "struct Code {\n"
       << "    static constexpr int N = " << sp.N << ";\n"
@@ -372,6 +412,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
           << "                                 typename P::v_t* wst, uint32_t* beta, const SyncT& sync) {\n"
           << "        constexpr bool NI = T == 32 && N >= 8192;  // shared non-inlined stage ops\n"
+          << "        PTRACE(0);\n"
           << body.str() << "    }\n";
     }
     o << "};\n\n}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
@@ -433,6 +474,11 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                  << "extern const unsigned polar_smem_" << sp.name << "_" << v.tag << ";\n";
     }
     std::ofstream(outdir + "/code_" + sp.name + ".cu") << o.str();
+    {
+        std::ofstream tl(outdir + "/trace_" + sp.name + ".txt");
+        for (auto& l : marks.labels) tl << l << "\n";
+    }
+    g_marks = nullptr;
 
     std::string sched;
     for (auto& s : ops) sched += s + ";";

@@ -55,6 +55,20 @@ PD_INLINE uint32_t h2max(uint32_t a, uint32_t b) {
 }
 
 PD_INLINE unsigned lane_id() { return threadIdx.x & 31u; }
+
+// POLAR_TRACE builds: clock64() after every op of the latency variant's critical path, block 0
+// thread 0 only, into the buffer the library passes (tools/trace_latency.py reads it back).
+#ifdef POLAR_TRACE
+static __device__ unsigned long long* g_ptrace;
+#define PTRACE(k)                                                                  \
+    do {                                                                           \
+        if (threadIdx.x == 0 && blockIdx.x == 0 && g_ptrace) g_ptrace[(k)] = clock64(); \
+    } while (0)
+#else
+#define PTRACE(k) \
+    do {          \
+    } while (0)
+#endif
 // Index of the thread in its frame group of T threads (T = 32: the lane).
 template <int T>
 PD_INLINE int gtid() { return T == 32 ? (int)(threadIdx.x & 31u) : (int)threadIdx.x; }

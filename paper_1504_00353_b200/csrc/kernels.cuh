@@ -98,6 +98,10 @@ __global__ void __launch_bounds__(T * FPC)
     const unsigned tid = FPC > 1 ? (threadIdx.x & 31u) : threadIdx.x;  // thread index in its group
     const bool leader = tid == 0;
 
+#ifdef POLAR_TRACE
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_ptrace = T > 32 ? (unsigned long long*)gscratch : nullptr;
+    __syncthreads();
+#endif
     // frames of round r: (r * gridDim.x + blockIdx.x) * FPC + grp
     const long long stride = (long long)gridDim.x * FPC;
     long long f = (long long)blockIdx.x * FPC + grp;

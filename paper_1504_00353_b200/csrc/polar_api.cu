@@ -64,6 +64,7 @@ struct polar_code {
     uint16_t* d_pos = nullptr;    // K information positions, ascending (encoder / generator)
     uint32_t* d_gtab = nullptr;   // gather table: info mask words, then info-bit prefix per word
     void* d_gscratch[4] = {nullptr, nullptr, nullptr, nullptr};  // per variant global stage scratch
+    unsigned long long* d_trace = nullptr;  // POLAR_TRACE builds: per-op clock64 of the latency variant
     uint32_t* d_info_mask = nullptr;  // N/32 words (>= 1), bit set = information position
     // host-buffer path (lazily allocated, guarded by mu)
     std::mutex mu;
@@ -129,6 +130,10 @@ static polar_status init_device(polar_code* h) {
     CUDA_TRY(cudaMemcpy(h->d_gtab, gt.data(), gt.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMalloc(&h->d_info_mask, im.size() * sizeof(uint32_t)));
     CUDA_TRY(cudaMemcpy(h->d_info_mask, im.data(), im.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+#ifdef POLAR_TRACE
+    CUDA_TRY(cudaMalloc(&h->d_trace, 65536 * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemset(h->d_trace, 0, 65536 * sizeof(unsigned long long)));
+#endif
     h->dev_ready = true;
     return POLAR_OK;
 }
@@ -171,6 +176,7 @@ extern "C" polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t*
 extern "C" void polar_code_destroy(polar_code* h) {
     if (!h) return;
     if (h->dev_ready) {
+        if (h->d_trace) cudaFree(h->d_trace);
         cudaFree(h->d_pos);
         cudaFree(h->d_info_mask);
         cudaFree(h->d_gtab);
@@ -221,6 +227,18 @@ extern "C" polar_status polar_code_schedule(const polar_code* h, char* buf, uint
     return POLAR_OK;
 }
 
+extern "C" polar_status polar_trace_fetch(const polar_code* h, uint64_t* host, uint32_t n) {
+    if (!h || !host) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
+#ifdef POLAR_TRACE
+    if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device");
+    CUDA_TRY(cudaMemcpy(host, h->d_trace, std::min<uint32_t>(n, 65536) * 8, cudaMemcpyDeviceToHost));
+    return POLAR_OK;
+#else
+    (void)n;
+    return fail(POLAR_ERR_UNSUPPORTED_CODE, "not a POLAR_TRACE build");
+#endif
+}
+
 extern "C" uint32_t polar_registry_size(void) { return kRegistrySize; }
 
 extern "C" polar_status polar_registry_entry(uint32_t i, uint32_t* N, uint32_t* K, uint8_t* mask_out) {
@@ -255,6 +273,9 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     long long nn = (long long)n;
     const uint32_t* gtab = h->d_gtab;
     void* gs = h->d_gscratch[vi];
+#ifdef POLAR_TRACE
+    if (lat) gs = h->d_trace;
+#endif
     void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs};
     CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(v.threads * v.frames), args, smem, s));
     return POLAR_OK;
