@@ -84,6 +84,7 @@ struct PF32 {
     using v_t = float;    // register value
     using acc_t = float;  // repetition accumulator
     static constexpr bool kExactSum = false;    // repetition sums in halving order (C13)
+    static constexpr bool kPackedKey = false;   // SPC argmin needs two reductions
     static constexpr bool kChanInSmem = false;  // N=32768 f32 channel does not fit with the tree
     static PD_INLINE v_t ld(float x) { return x; }
     static PD_INLINE float st(v_t x) { return x; }
@@ -112,6 +113,7 @@ struct PI8 {
     using v_t = float;
     using acc_t = float;
     static constexpr bool kExactSum = true;  // integer sums below 2^24: any order is exact (C12)
+    static constexpr bool kPackedKey = true;
     static constexpr bool kChanInSmem = true;
     // -128 -> -127 (C8); int -> float by the exponent trick (integer ALU + one FADD)
     static PD_INLINE v_t ld(int8_t x) { return __int_as_float(0x4B400000 + max((int)x, -127)) - 12582912.0f; }
@@ -299,8 +301,11 @@ PD_INLINE void group_sync() {
 
 // ------------------------------------------------------------------- warp-scope sources
 // A source of node LLRs: a register stage (RegSrc) or a shared-memory stage (MemSrc, the
-// subtree root).  v(j): element lane + 32 j (N_v >= 64).  one(n): element lane (N_v <= 32,
-// lanes >= n unspecified).  pair(h, x, y): elements lane and lane + h (N_v = 2h <= 32).
+// subtree root).  v(j): element lane + 32 j (N_v >= 64).  Nodes with N_v <= 32 are held
+// replicated: lane l holds element l mod N_v, so every lane carries a valid value and every
+// warp reduction below ends uniform without a broadcast.  one(n): element lane mod n.
+// pair(h, x, y) (node of 2h elements): x = own element (lane mod 2h), y = the partner
+// (lane mod 2h) xor h; lanes with (lane & h) hold the second element of their pair.
 
 template <class P>
 struct RegSrc {
@@ -310,7 +315,7 @@ struct RegSrc {
     PD_INLINE V one(int) const { return a[0]; }
     PD_INLINE void pair(int h, V& x, V& y) const {
         x = a[0];
-        y = __shfl_down_sync(FULL, a[0], h);
+        y = __shfl_xor_sync(FULL, a[0], h);
     }
 };
 
@@ -319,20 +324,18 @@ struct MemSrc {
     using V = typename P::v_t;
     const T* p;
     PD_INLINE V v(int j) const { return P::ld(p[lane_id() + 32 * j]); }
-    PD_INLINE V one(int n) const {
-        const unsigned l = lane_id();
-        return P::ld(p[l < (unsigned)n ? l : 0]);
-    }
+    PD_INLINE V one(int n) const { return P::ld(p[lane_id() & (n - 1)]); }
     PD_INLINE void pair(int h, V& x, V& y) const {
-        const unsigned l = lane_id() < (unsigned)h ? lane_id() : 0;
+        const unsigned l = lane_id() & (2 * h - 1);
         x = P::ld(p[l]);
-        y = P::ld(p[l + h]);
+        y = P::ld(p[l ^ h]);
     }
 };
 
 // ----------------------------------------------------------------- warp-scope operations
 
-// F<n>: child[i] = f(alpha[i], alpha[i + n/2]).
+// F<n>: child[i] = f(alpha[i], alpha[i + n/2]).  f is symmetric, so for n <= 32 both
+// lanes of a pair compute child element lane mod n/2 (the child stays replicated).
 template <class P, int n, class Src>
 PD_INLINE void wF(const Src& s, typename P::v_t* c) {
     if constexpr (n >= 64) {
@@ -356,11 +359,12 @@ PD_INLINE void wG(const Src& s, typename P::v_t* c, uint64_t bw, uint32_t ml) {
     } else {
         typename P::v_t x, y;
         s.pair(n / 2, x, y);
-        c[0] = P::g(x, y, (ml >> lane_id()) & 1u);
+        const bool second = lane_id() & (n / 2);
+        c[0] = P::g(second ? y : x, second ? x : y, (ml >> (lane_id() & (n / 2 - 1))) & 1u);
     }
 }
 
-// G_0R<n>: G with beta_l = 0 (left child Rate-0).
+// G_0R<n>: G with beta_l = 0 (left child Rate-0); b + a is symmetric.
 template <class P, int n, class Src>
 PD_INLINE void wG0R(const Src& s, typename P::v_t* c) {
     if constexpr (n >= 64) {
@@ -388,12 +392,13 @@ PD_INLINE uint32_t wR1m(const Src& s) {
 
 // Repetition<n>: all bits = [sum alpha < 0].  Sum in pairwise-halving order
 // x[i] += x[i + m/2], m = n, n/2, ..., 2 (reading C13): lane-local slot halving first, then
-// shuffles.  Returns the decision, uniform over the warp.
+// an xor butterfly over the lanes, which performs the same additions (each one commuted in
+// half of the lanes) and leaves the sum in every lane.
 template <class P, int n, class Src>
 PD_INLINE bool wRepDecide(const Src& s) {
     using A = typename P::acc_t;
     A t0;
-    int start;
+    constexpr int start = n >= 64 ? 16 : n / 2;
     if constexpr (n >= 64) {
         A t[n / 32];
 #pragma unroll
@@ -403,15 +408,12 @@ PD_INLINE bool wRepDecide(const Src& s) {
 #pragma unroll
             for (int j = 0; j < m / 2; ++j) t[j] = P::add(t[j], t[j + m / 2]);
         t0 = t[0];
-        start = 16;
     } else {
         t0 = P::acc(s.one(n));
-        start = n / 2;
     }
 #pragma unroll
-    for (int o = 16; o >= 1; o /= 2)
-        if (o <= start) t0 = P::add(t0, __shfl_down_sync(FULL, t0, o));
-    return __shfl_sync(FULL, (int)P::acc_neg(t0), 0) != 0;
+    for (int o = start; o >= 1; o /= 2) t0 = P::add(t0, __shfl_xor_sync(FULL, t0, o));
+    return P::acc_neg(t0);
 }
 template <class P, int n, int s0, class Src>
 PD_INLINE void wRep(const Src& s, uint64_t& bw) {
@@ -425,16 +427,23 @@ PD_INLINE uint32_t wRepm(const Src& s) {
 }
 
 // SPC<n>: hard decisions; if their parity is odd flip the decision of the
-// least reliable bit, the lowest index among equal magnitudes (reading C10).
+// least reliable bit, the lowest index among equal magnitudes (reading C10).  int8 profile:
+// the f32 bits of an integer magnitude <= 254 leave the low 16 mantissa bits zero, so
+// (|alpha| bits | index) is one exact key and one redux.min finds both minimum and index.
 template <class P, int n, class Src>
 PD_INLINE uint32_t wSPCm(const Src& s) {
     static_assert(n <= 32, "");
     const auto x = s.one(n);
     const uint32_t hdm = __ballot_sync(FULL, P::hd(x)) & low_mask(n);
     const uint32_t parity = __popc(hdm) & 1u;
-    const uint32_t key = lane_id() < (unsigned)n ? P::mag_key(x) : 0xffffffffu;
-    const uint32_t mn = __reduce_min_sync(FULL, key);
-    const uint32_t idx = __ffs(__ballot_sync(FULL, key == mn)) - 1;
+    uint32_t idx;
+    if constexpr (P::kPackedKey) {
+        idx = __reduce_min_sync(FULL, P::mag_key(x) | (lane_id() & (n - 1))) & 31u;
+    } else {
+        const uint32_t key = P::mag_key(x);
+        const uint32_t mn = __reduce_min_sync(FULL, key);
+        idx = __ffs(__ballot_sync(FULL, key == mn) & low_mask(n)) - 1;
+    }
     return hdm ^ (parity << idx);
 }
 template <class P, int n, int s0, class Src>
@@ -451,8 +460,13 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
         if (k < best) { best = k; bj = j; }
     }
     const uint32_t parity = __popc(__ballot_sync(FULL, __popcll(hb) & 1)) & 1u;
-    const uint32_t mn = __reduce_min_sync(FULL, best);
-    const uint32_t idx = __reduce_min_sync(FULL, best == mn ? bj * 32u + lane_id() : 0xffffffffu);
+    uint32_t idx;
+    if constexpr (P::kPackedKey) {
+        idx = __reduce_min_sync(FULL, best | (bj * 32u + lane_id())) & 0xffffu;
+    } else {
+        const uint32_t mn = __reduce_min_sync(FULL, best);
+        idx = __reduce_min_sync(FULL, best == mn ? bj * 32u + lane_id() : 0xffffffffu);
+    }
     if (parity && lane_id() == (idx & 31u)) hb ^= 1ull << (idx >> 5);
     bw |= hb << s0;
 }
@@ -584,8 +598,9 @@ PD_INLINE void cRep(const TS* __restrict__ src, TSc* scratch, uint32_t* beta) {
             __shared__ A red[T / 32];
             if (lane_id() == 0) red[gtid<T>() >> 5] = s;
             __syncthreads();
-            A tot = 0;  // exact: integer-valued, |sum| < 2^24
-            for (int w = 0; w < T / 32; ++w) tot = P::add(tot, red[w]);
+            A tot = lane_id() < T / 32 ? red[lane_id()] : A(0);  // exact: integer-valued, |sum| < 2^24
+#pragma unroll
+            for (int o = 16; o; o >>= 1) tot = P::add(tot, __shfl_xor_sync(FULL, tot, o));
             decision = P::acc_neg(tot);
         }
     } else {
@@ -633,11 +648,13 @@ PD_INLINE void cSPC(const TS* __restrict__ src, uint32_t* beta) {
             par[warp] = p;
         }
         __syncthreads();
-        p = 0;
-        for (int w = 0; w < T / 32; ++w) {
-            best = red[w] < best ? red[w] : best;
-            p ^= par[w];
+        best = lane_id() < T / 32 ? red[lane_id()] : ~0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(FULL, best, o);
+            best = other < best ? other : best;
         }
+        p = __popc(__ballot_sync(FULL, lane_id() < T / 32 ? (par[lane_id()] & 1u) : 0u)) & 1u;
     }
     group_sync<T>();
     if (gtid<T>() == 0 && p) {
