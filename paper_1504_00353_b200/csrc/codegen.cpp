@@ -45,6 +45,7 @@ struct Spec {
     int T = 512;    // threads per CTA in CTA mode
     int fpc_max = 16;  // most lockstep frames (warps) per CTA in the throughput variant
     std::set<int> dedup;  // sizes of subtrees shared as noinline functions (DEDUP=16,32,..)
+    int ll = 8;           // lane-local tiny subtrees up to this size (LL=0 disables)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
 };
 
@@ -61,6 +62,7 @@ struct TraceMarks {
     }
 };
 TraceMarks* g_marks = nullptr;
+int g_ll = 8;  // lane-local threshold of the code being emitted
 
 struct SharedFns {
     const std::vector<uint8_t>& mask;
@@ -87,12 +89,61 @@ struct Emitter {
     // subtree root.  src: the C++ expression of its LLR source.  Returns the name of the
     // uniform mask holding its beta when n <= 32, "" when beta was written into bw.
     std::string shared_fn(int id);
+    int ll = g_ll;  // split nodes (and repetition leaves) of size <= ll are decoded lane-locally
+
+    // Lane-local decode of node id whose n values are in register array `arr` (every lane
+    // holds all of them); returns the name of its beta mask.
+    int lane_blocks = 0;
+    std::string lane_pfx;
+    std::string lane(int id, const std::string& arr, int depth) {
+        const Node& v = t.nodes[id];
+        const int n = v.n;
+        const std::string N_ = std::to_string(n);
+        std::string m;
+        switch (v.kind) {
+            case Kind::Rate0: return "0u";
+            case Kind::Rate1: m = mask_name(); o << ind << "const uint32_t " << m << " = lR1<P, " << N_ << ">(" << arr << ");\n"; return m;
+            case Kind::Rep: m = mask_name(); o << ind << "const uint32_t " << m << " = lRep<P, " << N_ << ">(" << arr << ");\n"; return m;
+            case Kind::Spc: m = mask_name(); o << ind << "const uint32_t " << m << " = lSPC<P, " << N_ << ">(" << arr << ");\n"; return m;
+            case Kind::Split: break;
+        }
+        const int h = n / 2;
+        const std::string H = std::to_string(h);
+        const std::string c = lane_pfx + "q" + std::to_string(depth + 1) + "_" + std::to_string(next_mask);
+        o << ind << "V " << c << "[" << h << "];\n";
+        const Node& l = t.nodes[v.left];
+        const Node& r = t.nodes[v.right];
+        if (l.kind == Kind::Rate0) {
+            o << ind << "lG0R<P, " << N_ << ">(" << arr << ", " << c << ");\n";
+            std::string mr = lane(v.right, c, depth + 1);
+            m = mask_name();
+            o << ind << "const uint32_t " << m << " = " << mr << " | (" << mr << " << " << H << ");\n";
+            return m;
+        }
+        o << ind << "lF<P, " << N_ << ">(" << arr << ", " << c << ");\n";
+        std::string ml = lane(v.left, c, depth + 1);
+        if (r.kind == Kind::Rate0) return ml;
+        o << ind << "lG<P, " << N_ << ">(" << arr << ", " << c << ", " << ml << ");\n";
+        std::string mr = lane(v.right, c, depth + 1);
+        m = mask_name();
+        o << ind << "const uint32_t " << m << " = (" << ml << " ^ " << mr << ") | (" << mr << " << " << H << ");\n";
+        return m;
+    }
 
     std::string warp(int id, int off, const std::string& src, const std::string& src_arr = "") {
         const Node& v = t.nodes[id];
         const int n = v.n;
         const int s0 = off / 32;
         const std::string N_ = std::to_string(n), S0 = std::to_string(s0);
+        if (!src_arr.empty() && n <= ll && n >= 4 && (v.kind == Kind::Split || v.kind == Kind::Rep)) {
+            lane_pfx = "L" + std::to_string(lane_blocks++) + "_";
+            const std::string arr = lane_pfx + "q0";
+            o << ind << "V " << arr << "[" << n << "];\n";
+            o << ind << "lGather<P, " << N_ << ">(" << src_arr << "[0], " << arr << ");\n";
+            std::string m = lane(id, arr, 0);
+            mk("lane<" + N_ + ">");
+            return m;
+        }
         if (sh && v.kind == Kind::Split && !src_arr.empty() && sh->sizes.count(n) && id != body_root) {
             const std::string fn = shared_fn(id);
             std::string args;
@@ -372,6 +423,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     SharedFns sh{sp.mask, sp.dedup, {}, {}};
     TraceMarks marks;
     g_marks = &marks;
+    g_ll = sp.ll;
     marks.mark("start");
     std::ostringstream o;
     o << "struct Code {\n"
@@ -547,6 +599,7 @@ int main(int argc, char** argv) {
             else if (opt.rfind("T=", 0) == 0) sp.T = std::atoi(opt.c_str() + 2);
             else if (opt.rfind("FPC=", 0) == 0) sp.fpc_max = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("GS=", 0) == 0) sp.gs = std::atoi(opt.c_str() + 3);
+            else if (opt.rfind("LL=", 0) == 0) sp.ll = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();
                 std::stringstream ds(opt.substr(6));

@@ -471,6 +471,61 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
     bw |= hb << s0;
 }
 
+// ------------------------------------------------------- lane-local tiny subtrees (n <= 16)
+// A split node of a few elements is decoded inside every lane: its n values (replicated, lane
+// k holds element k) are gathered once with n independent shuffles, then the whole subtree
+// runs on compile-time-indexed registers with no further cross-lane latency; every lane
+// computes the same beta mask (bit i = beta[i]).  Same op order as the warp versions.
+template <class P, int n>
+PD_INLINE void lGather(typename P::v_t x, typename P::v_t* q) {
+#pragma unroll
+    for (int k = 0; k < n; ++k) q[k] = __shfl_sync(FULL, x, k);
+}
+template <class P, int n>
+PD_INLINE void lF(const typename P::v_t* a, typename P::v_t* c) {
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) c[i] = P::f(a[i], a[i + n / 2]);
+}
+template <class P, int n>
+PD_INLINE void lG(const typename P::v_t* a, typename P::v_t* c, uint32_t ml) {
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) c[i] = P::g(a[i], a[i + n / 2], (ml >> i) & 1u);
+}
+template <class P, int n>
+PD_INLINE void lG0R(const typename P::v_t* a, typename P::v_t* c) {
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) c[i] = P::g0(a[i], a[i + n / 2]);
+}
+template <class P, int n>
+PD_INLINE uint32_t lR1(const typename P::v_t* a) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) m |= (uint32_t)P::hd(a[i]) << i;
+    return m;
+}
+template <class P, int n>
+PD_INLINE uint32_t lRep(const typename P::v_t* a) {
+    typename P::acc_t t[n];
+#pragma unroll
+    for (int i = 0; i < n; ++i) t[i] = P::acc(a[i]);
+#pragma unroll
+    for (int m = n; m > 1; m /= 2)
+#pragma unroll
+        for (int i = 0; i < m / 2; ++i) t[i] = P::add(t[i], t[i + m / 2]);
+    return P::acc_neg(t[0]) ? low_mask(n) : 0u;
+}
+template <class P, int n>
+PD_INLINE uint32_t lSPC(const typename P::v_t* a) {
+    uint32_t h = 0, best = 0xffffffffu, idx = 0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) {
+        h |= (uint32_t)P::hd(a[i]) << i;
+        const uint32_t k = P::mag_key(a[i]);
+        if (k < best) { best = k; idx = i; }
+    }
+    return h ^ ((__popc(h) & 1u) << idx);
+}
+
 // Place the mask of a finished 32-bit node into bw slot s.
 template <int s>
 PD_INLINE void wDeposit(uint64_t& bw, uint32_t m) {
