@@ -45,7 +45,7 @@ struct Spec {
     int T = 512;    // threads per CTA in CTA mode
     int fpc_max = 16;  // most lockstep frames (warps) per CTA in the throughput variant
     std::set<int> dedup;  // sizes of subtrees shared as noinline functions (DEDUP=16,32,..)
-    int ll = 8;           // lane-local tiny subtrees up to this size (LL=0 disables)
+    int ll = 0;           // lane-local tiny subtrees up to this size (LL=8 enables; measured slower, profiles/r1_history.md)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
 };
 
@@ -62,7 +62,7 @@ struct TraceMarks {
     }
 };
 TraceMarks* g_marks = nullptr;
-int g_ll = 8;  // lane-local threshold of the code being emitted
+int g_ll = 0;  // lane-local threshold of the code being emitted
 
 struct SharedFns {
     const std::vector<uint8_t>& mask;
