@@ -149,6 +149,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1504_00353_b200 as pb
+    from paper_1504_00353_b200.shard import allreduce_counters, frame_range
 
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
@@ -160,17 +161,10 @@ def main():
         if ws > 1:
             dist.barrier()
 
-    def max_over_ranks(x: float) -> float:
-        if ws == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    from paper_1504_00353_b200.shard import max_over_ranks as _mor
 
-    def sum_over_ranks(t):
-        if ws > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return t
+    def max_over_ranks(x: float) -> float:
+        return _mor(x, dev)
 
     def throughput(code_t, B, steps, warmup, with_e2e):
         N, K, e = code_t
@@ -178,7 +172,8 @@ def main():
         llr = torch.empty(B, N, dtype=torch.int8, device=dev)
         truth = torch.empty(B, code.info_words, dtype=torch.int32, device=dev)
         out = torch.empty(B, code.info_words, dtype=torch.int32, device=dev)
-        code.gen_bpsk_awgn(SEED, rank * B, B, e, 4.0, llr_i8=llr, info=truth)
+        first, _ = frame_range(rank, ws, B)  # weak scaling: disjoint global frame ranges
+        code.gen_bpsk_awgn(SEED, first, B, e, 4.0, llr_i8=llr, info=truth)
         stream = torch.cuda.current_stream()
         for _ in range(warmup):
             code.decode_i8(llr, out)
@@ -202,7 +197,7 @@ def main():
         per_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
         ctr = torch.zeros(3, dtype=torch.int64, device=dev)
         code.count_errors(out, truth, ctr)
-        sum_over_ranks(ctr)
+        allreduce_counters(ctr)  # the one collective of the path
         frames, bit_err, frame_err = ctr.tolist()
         res = {"code": code, "N": N, "K": K, "B": B, "total_ms": total_ms, "ms_per_step": total_ms / steps,
                "launch_ms": per_launch_ms, "gbps": ws * B * K * steps / (total_ms * 1e-3) / 1e9,
@@ -269,6 +264,14 @@ def main():
     peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # T lane-ops/s
     achieved = elem * B / (main_r["launch_ms"] * 1e-3) / 1e12
     hbm_bytes = B * (N + 4 * code_words(K))
+    # DRAM bytes per frame measured by ncu (--set full) on the same kernel, scaled to this
+    # launch (profiles/traffic.json, written from the capture named there).
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        traffic = tj["c32768_29492_i8_tp"]["dram_bytes_per_frame"] * B
+    except (OSError, KeyError, ValueError):
+        pass
     line = {
         "metric": "info_gbps", "value": main_r["gbps"], "unit": "Gbps", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": main_r["ms_per_step"], "higher_is_better": True,
@@ -280,7 +283,8 @@ def main():
         "e2e": main_r["e2e"],
         "gpu_launches": args.steps,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (lane-ops)",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per frame x frames per launch)",
                      "hbm_achieved_gbs": hbm_bytes / (main_r["launch_ms"] * 1e-3) / 1e9,
                      "hbm_frac_of_measured": hbm_bytes / (main_r["launch_ms"] * 1e-3) / 1e9 / 6554.6},
         "clocks": main_r["clocks"],
