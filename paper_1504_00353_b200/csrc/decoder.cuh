@@ -137,8 +137,36 @@ struct PI8 {
 // stage ops can be shared non-inlined functions without falling back to generic accesses.
 enum : int { SP_GLOBAL = 0, SP_SHARED = 1 };
 
-template <int SP, int BYTES>
+// L2 eviction priority for global accesses: the channel is streamed (evict_first), the stage
+// scratch should stay resident (evict_last).
+enum : int { L2_NORMAL = 0, L2_FIRST = 1, L2_LAST = 2 };
+template <int H>
+PD_INLINE uint64_t l2_policy() {
+    uint64_t pol;
+    if constexpr (H == L2_FIRST) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+template <int SP, int BYTES, int H = L2_NORMAL>
 PD_INLINE void vld(const void* p, uint32_t* w) {
+#ifndef POLAR_L2_HINTS
+    static_assert(H == H, "");
+    constexpr int HH = L2_NORMAL;
+#else
+    constexpr int HH = H;
+#endif
+    if constexpr (SP == SP_GLOBAL && HH != L2_NORMAL) {
+        const uint64_t pol = l2_policy<HH>();
+        if constexpr (BYTES == 16)
+            asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                         : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "l"(p), "l"(pol));
+        else if constexpr (BYTES == 8)
+            asm volatile("ld.global.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(w[0]), "=r"(w[1]) : "l"(p), "l"(pol));
+        else
+            asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(w[0]) : "l"(p), "l"(pol));
+        return;
+    }
     if constexpr (SP == SP_SHARED) {
         const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
         if constexpr (BYTES == 16)
@@ -156,8 +184,25 @@ PD_INLINE void vld(const void* p, uint32_t* w) {
             asm volatile("ld.global.u32 %0, [%1];" : "=r"(w[0]) : "l"(p));
     }
 }
-template <int SP, int BYTES>
+template <int SP, int BYTES, int H = L2_NORMAL>
 PD_INLINE void vst(void* p, const uint32_t* w) {
+#ifndef POLAR_L2_HINTS
+    constexpr int HH = L2_NORMAL;
+#else
+    constexpr int HH = H;
+#endif
+    if constexpr (SP == SP_GLOBAL && HH != L2_NORMAL) {
+        const uint64_t pol = l2_policy<HH>();
+        if constexpr (BYTES == 16)
+            asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(w[0]), "r"(w[1]),
+                         "r"(w[2]), "r"(w[3]), "l"(pol) : "memory");
+        else if constexpr (BYTES == 8)
+            asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1,%2}, %3;" ::"l"(p), "r"(w[0]), "r"(w[1]), "l"(pol)
+                         : "memory");
+        else
+            asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(w[0]), "l"(pol) : "memory");
+        return;
+    }
     if constexpr (SP == SP_SHARED) {
         const uint32_t a = (uint32_t)__cvta_generic_to_shared(p);
         if constexpr (BYTES == 16)
@@ -183,17 +228,17 @@ template <int CE>
 struct Chunk<PF32, CE> {
     static_assert(CE == 4, "");
     float v[4];
-    template <int SP>
+    template <int SP, int H = L2_NORMAL>
     PD_INLINE void load(const void* p, bool = false) {
         uint32_t w[4];
-        vld<SP, 16>(p, w);
+        vld<SP, 16, H>(p, w);
 #pragma unroll
         for (int k = 0; k < 4; ++k) v[k] = __uint_as_float(w[k]);
     }
-    template <int SP, bool F32OUT>
+    template <int SP, bool F32OUT, int H = L2_NORMAL>
     PD_INLINE void store(void* p) const {
         const uint32_t w[4] = {__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])};
-        vst<SP, 16>(p, w);
+        vst<SP, 16, H>(p, w);
     }
 };
 
@@ -216,14 +261,14 @@ struct Chunk<PI8, CE> {
             }
         }
     }
-    template <int SP>
+    template <int SP, int H = L2_NORMAL>
     PD_INLINE void load(const void* p, bool clamp = false) {
         uint32_t w[CE / 4];
-        vld<SP, CE>(p, w);
+        vld<SP, CE, H>(p, w);
         unpack(w, clamp);
     }
     // F32OUT: the f32 stage feeding the register subtrees (latency variant), else int8
-    template <int SP, bool F32OUT>
+    template <int SP, bool F32OUT, int H = L2_NORMAL>
     PD_INLINE void store(void* p) const {
         if constexpr (F32OUT) {
 #pragma unroll
@@ -239,7 +284,7 @@ struct Chunk<PI8, CE> {
 #pragma unroll
             for (int q = 0; q < CE / 4; ++q)
                 w[q] = __byte_perm(h2add(h[2 * q], 0x64806480u), h2add(h[2 * q + 1], 0x64806480u), 0x6420) ^ 0x80808080u;
-            vst<SP, CE>(p, w);
+            vst<SP, CE, H>(p, w);
         }
     }
     // F: h = f(h, b)
@@ -581,10 +626,10 @@ PD_INLINE void cF_body(const void* src, void* dst) {
 #pragma unroll 4
     for (int i = CE * gtid<T>(); i < H; i += CE * T) {
         Chunk<P, CE> a, b;
-        a.template load<SS>((const S*)src + i, CLAMP);
-        b.template load<SS>((const S*)src + i + H, CLAMP);
+        a.template load<SS, CLAMP ? L2_FIRST : L2_LAST>((const S*)src + i, CLAMP);
+        b.template load<SS, CLAMP ? L2_FIRST : L2_LAST>((const S*)src + i + H, CLAMP);
         chunk_f(a, b);
-        a.template store<DS, F32OUT>((D*)dst + i);
+        a.template store<DS, F32OUT, L2_LAST>((D*)dst + i);
     }
 }
 template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, bool F32OUT>
@@ -595,11 +640,11 @@ PD_INLINE void cG_body(const void* src, void* dst, const uint32_t* beta) {
 #pragma unroll 4
     for (int i = CE * gtid<T>(); i < H; i += CE * T) {
         Chunk<P, CE> a, b;
-        a.template load<SS>((const S*)src + i, CLAMP);
-        b.template load<SS>((const S*)src + i + H, CLAMP);
+        a.template load<SS, CLAMP ? L2_FIRST : L2_LAST>((const S*)src + i, CLAMP);
+        b.template load<SS, CLAMP ? L2_FIRST : L2_LAST>((const S*)src + i + H, CLAMP);
         if constexpr (ZERO_LEFT) chunk_g0(a, b);
         else chunk_g(a, b, beta[i >> 5] >> (i & 31));
-        a.template store<DS, F32OUT>((D*)dst + i);
+        a.template store<DS, F32OUT, L2_LAST>((D*)dst + i);
     }
 }
 template <class P, int T, int n, bool CLAMP, int SS, int DS, bool F32OUT>
