@@ -228,10 +228,10 @@ template <int CE>
 struct Chunk<PF32, CE> {
     static_assert(CE == 4, "");
     float v[4];
+    uint32_t w[4];
     template <int SP, int H = L2_NORMAL>
-    PD_INLINE void load(const void* p, bool = false) {
-        uint32_t w[4];
-        vld<SP, 16, H>(p, w);
+    PD_INLINE void load_raw(const void* p) { vld<SP, 16, H>(p, w); }
+    PD_INLINE void unpack_raw(bool = false) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) v[k] = __uint_as_float(w[k]);
     }
@@ -261,12 +261,10 @@ struct Chunk<PI8, CE> {
             }
         }
     }
+    uint32_t w[CE / 4];
     template <int SP, int H = L2_NORMAL>
-    PD_INLINE void load(const void* p, bool clamp = false) {
-        uint32_t w[CE / 4];
-        vld<SP, CE, H>(p, w);
-        unpack(w, clamp);
-    }
+    PD_INLINE void load_raw(const void* p) { vld<SP, CE, H>(p, w); }
+    PD_INLINE void unpack_raw(bool clamp) { unpack(w, clamp); }
     // F32OUT: the f32 stage feeding the register subtrees (latency variant), else int8
     template <int SP, bool F32OUT, int H = L2_NORMAL>
     PD_INLINE void store(void* p) const {
@@ -618,33 +616,66 @@ PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
 // subtree-input stage.  Every distinct instance is one non-inlined function shared by all
 // call sites of the unrolled decoder (the stage ops are loops; inlining ~100 of them made
 // the N = 32768 kernels ~40% larger, profiles/r1_history.md).
+// Software-pipelined: the loads of U iterations are issued before any of their stores, so a
+// global (L2) stage keeps 2U 16-byte loads in flight per thread.
+template <class P, int H, int T>
+__host__ __device__ constexpr int stage_unroll() {
+    constexpr int step = chunk_elems<P, H, T>() * T;
+    constexpr int umax = T == 32 ? 4 : 2;  // the latency CTA runs under a 128-register cap
+    return H / step >= umax ? umax : H / step >= 2 ? 2 : 1;
+}
 template <class P, int T, int n, bool CLAMP, int SS, int DS, bool F32OUT>
 PD_INLINE void cF_body(const void* src, void* dst) {
     using S = typename P::st_t;
     using D = typename std::conditional<F32OUT, float, S>::type;
-    constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
-#pragma unroll 4
-    for (int i = CE * gtid<T>(); i < H; i += CE * T) {
-        Chunk<P, CE> a, b;
-        a.template load<SS, CLAMP ? L2_FIRST : L2_LAST>((const S*)src + i, CLAMP);
-        b.template load<SS, CLAMP ? L2_FIRST : L2_LAST>((const S*)src + i + H, CLAMP);
-        chunk_f(a, b);
-        a.template store<DS, F32OUT, L2_LAST>((D*)dst + i);
+    constexpr int H = n / 2, CE = chunk_elems<P, H, T>(), STEP = CE * T, U = stage_unroll<P, H, T>();
+    constexpr int LH = CLAMP ? L2_FIRST : L2_LAST;
+#pragma unroll 1
+    for (int i0 = CE * gtid<T>(); i0 < H; i0 += STEP * U) {
+        Chunk<P, CE> a[U], b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * STEP < H) {
+                a[u].template load_raw<SS, LH>((const S*)src + i0 + u * STEP);
+                b[u].template load_raw<SS, LH>((const S*)src + i0 + u * STEP + H);
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * STEP < H) {
+                a[u].unpack_raw(CLAMP);
+                b[u].unpack_raw(CLAMP);
+                chunk_f(a[u], b[u]);
+                a[u].template store<DS, F32OUT, L2_LAST>((D*)dst + i0 + u * STEP);
+            }
     }
 }
 template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, bool F32OUT>
 PD_INLINE void cG_body(const void* src, void* dst, const uint32_t* beta) {
     using S = typename P::st_t;
     using D = typename std::conditional<F32OUT, float, S>::type;
-    constexpr int H = n / 2, CE = chunk_elems<P, H, T>();
-#pragma unroll 4
-    for (int i = CE * gtid<T>(); i < H; i += CE * T) {
-        Chunk<P, CE> a, b;
-        a.template load<SS, CLAMP ? L2_FIRST : L2_LAST>((const S*)src + i, CLAMP);
-        b.template load<SS, CLAMP ? L2_FIRST : L2_LAST>((const S*)src + i + H, CLAMP);
-        if constexpr (ZERO_LEFT) chunk_g0(a, b);
-        else chunk_g(a, b, beta[i >> 5] >> (i & 31));
-        a.template store<DS, F32OUT, L2_LAST>((D*)dst + i);
+    constexpr int H = n / 2, CE = chunk_elems<P, H, T>(), STEP = CE * T, U = stage_unroll<P, H, T>();
+    constexpr int LH = CLAMP ? L2_FIRST : L2_LAST;
+#pragma unroll 1
+    for (int i0 = CE * gtid<T>(); i0 < H; i0 += STEP * U) {
+        Chunk<P, CE> a[U], b[U];
+        uint32_t bits[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * STEP < H) {
+                const int i = i0 + u * STEP;
+                a[u].template load_raw<SS, LH>((const S*)src + i);
+                b[u].template load_raw<SS, LH>((const S*)src + i + H);
+                bits[u] = ZERO_LEFT ? 0u : beta[i >> 5] >> (i & 31);
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * STEP < H) {
+                a[u].unpack_raw(CLAMP);
+                b[u].unpack_raw(CLAMP);
+                if constexpr (ZERO_LEFT) chunk_g0(a[u], b[u]);
+                else chunk_g(a[u], b[u], bits[u]);
+                a[u].template store<DS, F32OUT, L2_LAST>((D*)dst + i0 + u * STEP);
+            }
     }
 }
 template <class P, int T, int n, bool CLAMP, int SS, int DS, bool F32OUT>
