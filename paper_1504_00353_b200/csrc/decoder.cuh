@@ -621,7 +621,7 @@ PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
 template <class P, int H, int T>
 __host__ __device__ constexpr int stage_unroll() {
     constexpr int step = chunk_elems<P, H, T>() * T;
-    constexpr int umax = T == 32 ? 4 : 2;  // the latency CTA runs under a 128-register cap
+    constexpr int umax = T == 32 ? 4 : 1;  // the latency CTA (shared-memory stages, 128-register cap) needs none
     return H / step >= umax ? umax : H / step >= 2 ? 2 : 1;
 }
 template <class P, int T, int n, bool CLAMP, int SS, int DS, bool F32OUT>
