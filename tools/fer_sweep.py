@@ -1,0 +1,128 @@
+"""FER / BER sweep (BASELINE config 4) and batch-size throughput sweep (config 5).
+
+  python tools/fer_sweep.py fer   [--code 32768,27568 --design 4.0 --points 3.5,3.75,4.0,4.25 ...]
+  python tools/fer_sweep.py batch [--code 2048,1723 --design 4.0 --max-log4 11]
+
+fer: for each Eb/N0 point, decode seeded frames (device generator, mask fixed at the design
+Eb/N0, reading C1) in chunks until `--errors` frame errors or `--max-frames`; every frame the GPU
+decodes wrongly plus `--check` random frames per point are re-decoded by the CPU oracle (O2)
+and must match bit for bit; prints FER/BER with Clopper-Pearson 95% intervals next to the GA
+closed-form estimate 1 - prod(1 - Q(sqrt(m_i / 2))) over the information set (SURVEY 8(c) pin 9).
+batch: info Gbps and frames/s of the int8 decoder for batches 4^0 .. 4^max (CUDA events).
+Writes one JSON line per point to stdout.
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from scipy.stats import beta as beta_dist  # noqa: E402
+
+import oracle  # noqa: E402  (test/measurement infrastructure: the checker)
+import paper_1504_00353_b200 as pb  # noqa: E402
+
+SEED = 1504000353
+
+
+def clopper_pearson(k, n, a=0.05):
+    lo = 0.0 if k == 0 else beta_dist.ppf(a / 2, k, n - k + 1)
+    hi = 1.0 if k == n else beta_dist.ppf(1 - a / 2, k + 1, n - k)
+    return lo, hi
+
+
+def ga_fer(N, K, design, ebn0):
+    mask = oracle.construct_ga(N, K, design)
+    m = oracle.ga_means(N, K, ebn0)[mask == 0]
+    q = 0.5 * np.array([math.erfc(math.sqrt(x / 2) / math.sqrt(2)) for x in m])
+    return float(1.0 - np.prod(1.0 - q))
+
+
+def fer(a):
+    N, K = map(int, a.code.split(","))
+    code = pb.PolarCode.ga(N, K, a.design)
+    mask = code.mask()
+    W = code.info_words
+    chunk = a.chunk
+    llr8 = torch.empty(chunk, N, dtype=torch.int8, device="cuda")
+    llr32 = torch.empty(chunk, N, dtype=torch.float32, device="cuda") if a.f32 else None
+    truth = torch.empty(chunk, W, dtype=torch.int32, device="cuda")
+    out = torch.empty(chunk, W, dtype=torch.int32, device="cuda")
+    rng = np.random.default_rng(7)
+    for e in [float(x) for x in a.points.split(",")]:
+        for prof in (["i8", "f32"] if a.f32 else ["i8"]):
+            frames = bit_err = frame_err = checked = 0
+            first = 0
+            t0 = time.time()
+            while frame_err < a.errors and frames < a.max_frames:
+                n = min(chunk, a.max_frames - frames)
+                code.gen_bpsk_awgn(SEED, first, n, e, 4.0, llr_f32=llr32[:n] if prof == "f32" else None,
+                                   llr_i8=llr8[:n] if prof == "i8" else None, info=truth[:n])
+                x = llr8[:n] if prof == "i8" else llr32[:n]
+                (code.decode_i8 if prof == "i8" else code.decode_f32)(x, out[:n])
+                d = (out[:n] ^ truth[:n]).cpu().numpy().view(np.uint32)
+                bad = np.flatnonzero(d.any(axis=1))
+                frame_err += len(bad)
+                bit_err += int(np.unpackbits(d.view(np.uint8)).sum())
+                # oracle re-decode of the GPU's error frames and of a random sample
+                idx = np.union1d(bad[: a.check], rng.choice(n, min(a.check, n), replace=False))
+                sample = x[torch.from_numpy(idx).cuda()].cpu().numpy()
+                want = oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, sample, threads=os.cpu_count())))
+                got = out[:n][torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint32)
+                if not np.array_equal(got, want):
+                    raise SystemExit(f"PARITY FAILURE at {e} dB {prof}: {int((got != want).any(axis=1).sum())} frames")
+                checked += len(idx)
+                frames += n
+                first += n
+            lo, hi = clopper_pearson(frame_err, frames)
+            print(json.dumps({"code": [N, K], "design_ebn0": a.design, "ebn0": e, "profile": prof, "frames": frames,
+                              "frame_errors": frame_err, "fer": frame_err / frames, "fer_ci95": [lo, hi],
+                              "ber": bit_err / (frames * K), "ga_fer": ga_fer(N, K, a.design, e),
+                              "oracle_checked_frames": checked, "seconds": round(time.time() - t0, 2)}), flush=True)
+
+
+def batch(a):
+    N, K = map(int, a.code.split(","))
+    code = pb.PolarCode.ga(N, K, a.design)
+    W = code.info_words
+    nmax = 4 ** a.max_log4
+    llr = torch.empty(nmax, N, dtype=torch.int8, device="cuda")
+    code.gen_bpsk_awgn(SEED, 0, nmax, a.design, 4.0, llr_i8=llr)
+    out = torch.empty(nmax, W, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream()
+    for k in range(a.max_log4 + 1):
+        n = 4 ** k
+        for _ in range(3):
+            code.decode_i8(llr[:n], out[:n])
+        reps = max(3, min(200, (1 << 22) // n))
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(s)
+        for _ in range(reps):
+            code.decode_i8(llr[:n], out[:n])
+        ev1.record(s)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / reps
+        print(json.dumps({"code": [N, K], "batch": n, "ms": ms, "frames_per_s": n / (ms * 1e-3),
+                          "info_gbps": n * K / (ms * 1e-3) / 1e9,
+                          "variant": "latency" if n <= torch.cuda.get_device_properties(0).multi_processor_count else "throughput"}),
+              flush=True)
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", choices=["fer", "batch"])
+    ap.add_argument("--code", default="32768,27568")
+    ap.add_argument("--design", type=float, default=4.0)
+    ap.add_argument("--points", default="3.5,3.75,4.0,4.25")
+    ap.add_argument("--errors", type=int, default=100)
+    ap.add_argument("--max-frames", type=int, default=20_000_000)
+    ap.add_argument("--chunk", type=int, default=65536)
+    ap.add_argument("--check", type=int, default=64)
+    ap.add_argument("--f32", action="store_true")
+    ap.add_argument("--max-log4", type=int, default=8)
+    a = ap.parse_args()
+    (fer if a.mode == "fer" else batch)(a)
