@@ -80,8 +80,8 @@ polar_status polar_code_query(const polar_code* h, uint32_t* N, uint32_t* K, uin
 polar_status polar_code_schedule(const polar_code* h, char* buf, uint32_t cap, uint32_t* needed);
 
 /* Kernel variant used by the decode calls: 0 = automatic (default: the latency variant,
- * one CTA per frame, when n_frames <= number of SMs, else the throughput variant, one warp
- * per frame), 1 = always throughput, 2 = always latency.  Both decode identically.  Not
+ * one CTA per frame, when n_frames <= number of SMs (x4 for N >= 16384), else the throughput
+ * variant, one warp per frame), 1 = always throughput, 2 = always latency.  Both decode identically.  Not
  * thread-safe with concurrent decode calls on the same handle. */
 polar_status polar_code_set_variant(polar_code* h, int variant);
 

@@ -263,7 +263,10 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     const RegistryEntry* e = h->entry;
     // Latency variant (a CTA per frame) for batches that cannot fill the GPU with one frame
     // per warp; otherwise the throughput variant (a warp per frame).
-    const bool lat = h->variant == 2 || (h->variant == 0 && n <= (int64_t)h->n_sm);
+    // (measured crossover, profiles/r1_sweeps.md: at N >= 16384 one latency wave of #SMs
+    // frames takes ~1/4 of a throughput wave)
+    const int64_t lat_max = (int64_t)h->n_sm * (h->N >= 16384 ? 4 : 1);
+    const bool lat = h->variant == 2 || (h->variant == 0 && n <= lat_max);
     const int vi = (lat ? 2 : 0) + (i8 ? 1 : 0);
     const Variant& v = vi == 0 ? e->tp_f32 : vi == 1 ? e->tp_i8 : vi == 2 ? e->lat_f32 : e->lat_i8;
     const void* kern = *v.kern;
