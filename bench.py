@@ -46,33 +46,66 @@ def _dist():
 
 
 class Clocks:
-    """Samples nvidia-smi clocks and throttle reasons during the timed region."""
+    """Samples SM clocks and throttle reasons during the timed region: NVML in-process every
+    5 ms (the timed region is tens of ms), nvidia-smi as a fallback."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
-        self.index, self.rows, self._p = index, [], None
-
-    def __enter__(self):
+        self.index, self.rows, self._stop = index, [], threading.Event()
+        self._nv = None
         try:
-            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                        "--format=csv,noheader,nounits", "-lms", "100"],
-                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
-            self._t.start()
-        except FileNotFoundError:
-            self._p = None
-        return self
+            import pynvml
 
-    def _read(self):
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._masks = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                           pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _poll(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.rows.append((float(sm), float(self._max), [bool(r & m) for m in self._masks]))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def _read_smi(self):
         for line in self._p.stdout:
             f = [x.strip() for x in line.split(",")]
-            if len(f) == 6:
-                self.rows.append(f)
+            if len(f) == 6 and f[0].replace(".", "").isdigit():
+                self.rows.append((float(f[0]), float(f[1]), [x.lower() == "active" for x in f[2:6]]))
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._poll, daemon=True)
+            self._t.start()
+            return self
+        self._p = None
+        try:
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                        "--format=csv,noheader,nounits", "-lms", "100"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read_smi, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            pass
+        return self
 
     def __exit__(self, *a):
-        if self._p:
+        if self._nv is not None:
+            self._stop.set()
+            self._t.join()
+        elif self._p:
             time.sleep(0.15)
             self._p.terminate()
             self._p.wait()
@@ -80,12 +113,10 @@ class Clocks:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if r[2][i]})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows), "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml" if self._nv is not None else "nvidia-smi"}
 
 
 def cpu_oracle_rate(N, K, e, sample_frames, threads, seconds_cap=20.0):
