@@ -404,6 +404,12 @@ PD_INLINE void wG(const Src& s, typename P::v_t* c, uint64_t bw, uint32_t ml) {
         // (partner, own) in the second: flip the sign of own (first half) or of the partner
         // (second half), then add -- the masks depend only on ml and the lane, so the
         // critical path after the shuffle is xor, add, saturate.
+#ifdef POLAR_SELECT_SMALL_G
+        typename P::v_t x, y;
+        s.pair(n / 2, x, y);
+        const bool second = lane_id() & (n / 2);
+        c[0] = P::g(second ? y : x, second ? x : y, (ml >> (lane_id() & (n / 2 - 1))) & 1u);
+#else
         const uint32_t sgn = ((ml >> (lane_id() & (n / 2 - 1))) & 1u) << 31;
         const uint32_t second = (lane_id() & (n / 2)) ? 0xffffffffu : 0u;
         typename P::v_t x, y;
@@ -411,6 +417,7 @@ PD_INLINE void wG(const Src& s, typename P::v_t* c, uint64_t bw, uint32_t ml) {
         const float xa = __uint_as_float(__float_as_uint(x) ^ (sgn & ~second));
         const float ya = __uint_as_float(__float_as_uint(y) ^ (sgn & second));
         c[0] = P::g0(xa, ya);
+#endif
     }
 }
 
