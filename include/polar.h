@@ -31,7 +31,7 @@ extern "C" {
 typedef enum polar_status {
     POLAR_OK = 0,
     POLAR_ERR_INVALID_ARGUMENT = 1, /* bad size, null or misaligned pointer, bad mask   */
-    POLAR_ERR_UNSUPPORTED_CODE = 2, /* no kernel was specialised for this (N, K, mask)  */
+    POLAR_ERR_UNSUPPORTED_CODE = 2, /* operation not available for this code or build   */
     POLAR_ERR_CUDA = 3,             /* a CUDA runtime call or kernel launch failed      */
     POLAR_ERR_OUT_OF_MEMORY = 4
 } polar_status;
@@ -55,11 +55,12 @@ const char* polar_last_error(void);
  *   frozen_mask  host, N bytes, 1 = frozen, natural indexing; exactly N-K
  *                entries must be 1.  The library copies it.
  *   out          receives the handle.
- * The frozen set must be one of the sets the library was specialised for at build time
- * (the decoders are fully unrolled per code); otherwise
- * POLAR_ERR_UNSUPPORTED_CODE.  Host-side only, except a one-time upload of the K-entry
- * information-position table; without a CUDA device the handle is still created (query
- * and schedule work) and the device calls return POLAR_ERR_CUDA. */
+ * Frozen sets the library was specialised for at build time get the unrolled decoders
+ * (P:637-656); any other frozen set gets the generic, program-interpreted decoder
+ * (the paper's instruction-based decoder: same results, lower throughput; see
+ * polar_code_is_specialised).  Host-side only, except one-time uploads of small tables;
+ * without a CUDA device the handle is still created (query and schedule work) and the
+ * device calls return POLAR_ERR_CUDA. */
 polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t* frozen_mask,
                                polar_code** out);
 
@@ -78,6 +79,10 @@ polar_status polar_code_query(const polar_code* h, uint32_t* N, uint32_t* K, uin
  * ';'-separated ("F<8>;G_0R<4>;Info<2>;...").  Writes at most cap bytes including the
  * terminating NUL into buf (may be NULL); *needed (may be NULL) receives the full size. */
 polar_status polar_code_schedule(const polar_code* h, char* buf, uint32_t cap, uint32_t* needed);
+
+/* *specialised = 1 if the handle uses a decoder unrolled for its code at build time, 0 if it
+ * uses the generic program-interpreted decoder. */
+polar_status polar_code_is_specialised(const polar_code* h, int* specialised);
 
 /* Kernel variant used by the decode calls: 0 = automatic (default: the latency variant,
  * one CTA per frame, when n_frames <= number of SMs (x4 for N >= 16384), else the throughput

@@ -25,7 +25,8 @@ POLAR_ERR_OUT_OF_MEMORY = 4
 # Every symbol include/polar.h declares (checked by tests/test_abi.py).
 EXPORTS = [
     "polar_status_string", "polar_last_error", "polar_code_create", "polar_code_destroy",
-    "polar_code_query", "polar_code_schedule", "polar_code_mask", "polar_code_set_variant", "polar_decode_f32",
+    "polar_code_query", "polar_code_schedule", "polar_code_mask", "polar_code_set_variant",
+    "polar_code_is_specialised", "polar_decode_f32",
     "polar_decode_i8", "polar_decode_f32_host", "polar_decode_i8_host", "polar_construct_ga",
     "polar_encode_systematic", "polar_gen_bpsk_awgn", "polar_count_errors",
     "polar_registry_size", "polar_registry_entry", "polar_trace_fetch",
@@ -59,6 +60,7 @@ def lib() -> C.CDLL:
         "polar_code_schedule": (C.c_int, [vp, C.c_char_p, C.c_uint32, u32p]),
         "polar_code_mask": (C.c_int, [vp, vp]),
         "polar_code_set_variant": (C.c_int, [vp, C.c_int]),
+        "polar_code_is_specialised": (C.c_int, [vp, C.POINTER(C.c_int)]),
         "polar_decode_f32": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
         "polar_decode_i8": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
         "polar_decode_f32_host": (C.c_int, [vp, vp, C.c_int64, vp]),
@@ -137,6 +139,9 @@ class PolarCode:
         _check(lib().polar_code_query(h, C.byref(n), C.byref(k), C.byref(ops), C.byref(smem), C.byref(wr)))
         self.N, self.K, self.n_ops, self.smem_bytes, self.warp_root = n.value, k.value, ops.value, smem.value, wr.value
         self.info_words = (self.K + 31) // 32
+        sp = C.c_int()
+        _check(lib().polar_code_is_specialised(h, C.byref(sp)))
+        self.specialised = bool(sp.value)
 
     @classmethod
     def ga(cls, N: int, K: int, design_ebn0_db: float) -> "PolarCode":
@@ -154,8 +159,8 @@ class PolarCode:
             pass
 
     def set_variant(self, variant: str) -> None:
-        """'auto' | 'throughput' | 'latency' (both kernels decode identically)."""
-        _check(lib().polar_code_set_variant(self._h, {"auto": 0, "throughput": 1, "latency": 2}[variant]))
+        """'auto' | 'throughput' | 'latency' | 'generic' (all decode identically)."""
+        _check(lib().polar_code_set_variant(self._h, {"auto": 0, "throughput": 1, "latency": 2, "generic": 3}[variant]))
 
     def mask(self) -> np.ndarray:
         m = np.zeros(self.N, np.uint8)

@@ -98,6 +98,7 @@ def build(verbose: bool = True, jobs: int | None = None) -> str:
     shutil.rmtree(scratch)
     # 3. compile
     units = [(os.path.join(CSRC, "polar_api.cu"), "polar_api.o"),
+             (os.path.join(CSRC, "generic.cu"), "generic.o"),
              (os.path.join(CSRC, "construct.cpp"), "construct.o"),
              (os.path.join(GEN, "registry.cpp"), "registry.o")]
     units += [(os.path.join(GEN, fn), fn[:-3] + ".o") for fn in sorted(new) if fn.endswith(".cu")]

@@ -1,0 +1,181 @@
+// generic.cu -- the program-interpreted Fast-SSC decoder for any frozen set (N <= 32768).
+//
+// The paper has two decoder builders: the unrolled decoder generated per code (P:633-864,
+// our build-time specialisation) and the instruction-based decoder that reads the list of
+// operations at run time.  This is the latter: polar_code_create
+// falls back to it for frozen sets no decoder was specialised for, so the ABI accepts every
+// (N, K, mask).  One warp per frame, all stages in shared memory (stage(m) at N - 2m), beta
+// as the natural bit array; the op list is tree.hpp::program().  Same f/g/leaf arithmetic
+// and op order as the specialised kernels (decoder.cuh), so results are identical.
+#include "decoder.cuh"
+#include "tree.hpp"
+
+namespace pd {
+using namespace polar;  // OP_* opcodes of tree.hpp
+
+__host__ __device__ inline int g_align16(int x) { return (x + 15) & ~15; }
+
+template <class P>
+__host__ __device__ inline int generic_smem(int N, int K) {
+    const int stages = g_align16((N > 1 ? N - 1 : 1) * (int)sizeof(typename P::st_t));
+    const int nb = N >= 32 ? N / 32 : 1;
+    return stages + 4 * nb + 4 * ((K + 31) / 32) + 16;
+}
+
+// Write n < 32 bits (LSB-first) into the natural bit array at bit `off` (one word).
+PD_INLINE void put_bits(uint32_t* beta, int off, int n, uint32_t bits) {
+    const uint32_t m = low_mask(n) << (off & 31);
+    uint32_t& w = beta[off >> 5];
+    w = (w & ~m) | ((bits << (off & 31)) & m);
+}
+
+template <class P>
+__global__ void __launch_bounds__(32) k_generic(const void* __restrict__ llr_, long long n_frames,
+                                                uint32_t* __restrict__ out, const uint32_t* __restrict__ gtab,
+                                                const uint32_t* __restrict__ prog, int n_ops, int N, int K) {
+    using S = typename P::st_t;
+    using V = typename P::v_t;
+    extern __shared__ __align__(16) unsigned char gsmem[];
+    S* const st = (S*)gsmem;
+    const int NB = N >= 32 ? N / 32 : 1;
+    const int NWK = (K + 31) / 32;
+    uint32_t* const beta = (uint32_t*)(gsmem + g_align16((N > 1 ? N - 1 : 1) * (int)sizeof(S)));
+    uint32_t* const stg = beta + NB;
+    const S* llr = (const S*)llr_;
+    const int l = lane_id();
+    for (long long f = blockIdx.x; f < n_frames; f += gridDim.x) {
+        const S* chan = llr + f * N;
+        for (int k = l; k < NB; k += 32) beta[k] = 0;
+        __syncwarp();
+        for (int pc = 0; pc < n_ops; ++pc) {
+            const uint32_t w = __ldg(prog + pc);
+            const int op = w & 15, n = 1 << ((w >> 4) & 31), off = (int)(w >> 9), h = n >> 1;
+            const S* src = n == N ? chan : st + (N - 2 * n);
+            S* dst = st + (N - n);  // stage(n/2)
+            switch (op) {
+                case OP_F:
+                    for (int i = l; i < h; i += 32) dst[i] = P::st(P::f(P::ld(src[i]), P::ld(src[i + h])));
+                    break;
+                case OP_G:
+                    for (int i = l; i < h; i += 32)
+                        dst[i] = P::st(P::g(P::ld(src[i]), P::ld(src[i + h]), (beta[(off + i) >> 5] >> ((off + i) & 31)) & 1u));
+                    break;
+                case OP_G0R:
+                    for (int i = l; i < h; i += 32) dst[i] = P::st(P::g0(P::ld(src[i]), P::ld(src[i + h])));
+                    break;
+                case OP_R1:
+                    for (int i0 = 0; i0 < n; i0 += 32) {
+                        const uint32_t b = __ballot_sync(FULL, i0 + l < n && P::hd(P::ld(src[i0 + l])));
+                        if (l == 0) {
+                            if (n >= 32) beta[(off + i0) >> 5] = b;
+                            else put_bits(beta, off, n, b);
+                        }
+                    }
+                    break;
+                case OP_REP: {
+                    // repetition: the decision is [sum < 0]
+                    bool neg;
+                    if constexpr (P::kExactSum) {  // int8: exact, any order (reading C12)
+                        typename P::acc_t t = 0;
+                        for (int i = l; i < n; i += 32) t = P::add(t, P::acc(P::ld(src[i])));
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) t = P::add(t, __shfl_xor_sync(FULL, t, o));
+                        neg = P::acc_neg(t);
+                    } else {  // f32: pairwise halving order (reading C13)
+                        typename P::acc_t t;
+                        int start;
+                        if (n <= 32) {
+                            t = P::acc(P::ld(src[l & (n - 1)]));
+                            start = h;
+                        } else {
+                            for (int i = l; i < h; i += 32) dst[i] = P::add(P::ld(src[i]), P::ld(src[i + h]));
+                            __syncwarp();
+                            for (int m = h; m > 32; m >>= 1) {
+                                for (int i = l; i < m / 2; i += 32) dst[i] = P::add(dst[i], dst[i + m / 2]);
+                                __syncwarp();
+                            }
+                            t = dst[l];
+                            start = 16;
+                        }
+                        for (int o = start; o >= 1; o >>= 1) t = P::add(t, __shfl_xor_sync(FULL, t, o));
+                        neg = P::acc_neg(t);
+                    }
+                    if (n >= 32) {
+                        for (int k = l; k < n / 32; k += 32) beta[(off >> 5) + k] = neg ? FULL : 0u;
+                    } else if (l == 0) {
+                        put_bits(beta, off, n, neg ? FULL : 0u);
+                    }
+                    break;
+                }
+                case OP_SPC: {
+                    // SPC: hard decisions, parity, flip the lowest-index least
+                    // magnitude when the parity is odd (readings C10, C11)
+                    uint32_t par = 0, best = 0xffffffffu, bi = 0xffffffffu;
+                    for (int i0 = 0; i0 < n; i0 += 32) {
+                        const int i = i0 + l;
+                        const bool in = i < n;
+                        const V x = in ? P::ld(src[i]) : V(0);
+                        const uint32_t b = __ballot_sync(FULL, in && P::hd(x));
+                        par ^= __popc(b) & 1u;
+                        if (l == 0) {
+                            if (n >= 32) beta[(off + i0) >> 5] = b;
+                            else put_bits(beta, off, n, b);
+                        }
+                        const uint32_t k = in ? P::mag_key(x) : 0xffffffffu;
+                        if (k < best) { best = k; bi = i; }
+                    }
+                    uint32_t idx;
+                    if constexpr (P::kPackedKey) {
+                        idx = __reduce_min_sync(FULL, best == 0xffffffffu ? best : (best | bi)) & 0xffffu;
+                    } else {
+                        const uint32_t mn = __reduce_min_sync(FULL, best);
+                        idx = __reduce_min_sync(FULL, best == mn ? bi : 0xffffffffu);
+                    }
+                    __syncwarp();
+                    if (l == 0 && par) beta[(off + idx) >> 5] ^= 1u << ((off + idx) & 31);
+                    break;
+                }
+                case OP_COMB:
+                case OP_COMB0R:
+                    if (n >= 64) {
+                        for (int k = l; k < n / 64; k += 32) {
+                            const uint32_t r = beta[(off >> 5) + n / 64 + k];
+                            beta[(off >> 5) + k] = op == OP_COMB ? beta[(off >> 5) + k] ^ r : r;
+                        }
+                    } else if (l == 0) {
+                        const uint32_t wv = beta[off >> 5];
+                        const uint32_t r = (wv >> ((off & 31) + h)) & low_mask(h);
+                        const uint32_t left = op == OP_COMB ? ((wv >> (off & 31)) & low_mask(h)) ^ r : r;
+                        put_bits(beta, off, h, left);
+                    }
+                    break;
+            }
+            __syncwarp();
+        }
+        // systematic information bits x_hat[A] (as gather_info, runtime sizes)
+        for (int q = l; q < NWK; q += 32) stg[q] = 0;
+        __syncwarp();
+        for (int k = l; k < NB; k += 32) {
+            const uint32_t m = __ldg(gtab + k);
+            if (!m) continue;
+            const uint32_t p = __ldg(gtab + NB + k);
+            const uint32_t r = pext32(beta[k], m);
+            const uint32_t sh = p & 31;
+            atomicOr(stg + (p >> 5), r << sh);
+            if (sh && sh + __popc(m) > 32) atomicOr(stg + (p >> 5) + 1, r >> (32 - sh));
+        }
+        __syncwarp();
+        for (int q = l; q < NWK; q += 32) out[f * NWK + q] = stg[q];
+        __syncwarp();
+    }
+}
+
+}  // namespace pd
+
+// Entry points for polar_api.cu (kernel addresses and shared-memory sizes).
+const void* polar_generic_kernel(bool i8) {
+    return i8 ? (const void*)&pd::k_generic<pd::PI8> : (const void*)&pd::k_generic<pd::PF32>;
+}
+int polar_generic_smem(bool i8, int N, int K) {
+    return i8 ? pd::generic_smem<pd::PI8>(N, K) : pd::generic_smem<pd::PF32>(N, K);
+}

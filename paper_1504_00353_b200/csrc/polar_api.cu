@@ -22,6 +22,9 @@
 namespace polar {
 void construct_ga(int N, int K, double design_ebn0_db, uint8_t* frozen);
 }
+// generic.cu: the program-interpreted decoder for frozen sets without a specialised kernel
+const void* polar_generic_kernel(bool i8);
+int polar_generic_smem(bool i8, int N, int K);
 
 using namespace polar;
 
@@ -52,7 +55,11 @@ static polar_status fail(polar_status s, const char* fmt, ...) {
 struct polar_code {
     uint32_t N = 0, K = 0;
     std::vector<uint8_t> mask;
-    const RegistryEntry* entry = nullptr;
+    const RegistryEntry* entry = nullptr;  // specialised decoder, or nullptr: generic
+    std::vector<uint32_t> prog;             // generic decoder: the op program (tree.hpp)
+    std::string sched;                      // Listing-1 op list
+    uint32_t* d_prog = nullptr;
+    int occ_generic[2] = {0, 0};
     uint32_t n_ops = 0;
     bool systematic_ok = false;  // information set closed under bit-superset (reading C4)
     // device side (absent when no usable device at create time)
@@ -99,8 +106,25 @@ static polar_status init_device(polar_code* h) {
     CUDA_TRY(cudaGetDevice(&h->device));
     CUDA_TRY(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
     const RegistryEntry* e = h->entry;
-    const Variant* vs[4] = {&e->tp_f32, &e->tp_i8, &e->lat_f32, &e->lat_i8};
-    for (int i = 0; i < 4; ++i) {
+    {  // generic decoder (any code): one warp per frame, all stages in shared memory
+        for (int i = 0; i < 2; ++i) {
+            const void* k = polar_generic_kernel(i == 1);
+            const int sm = polar_generic_smem(i == 1, (int)h->N, (int)h->K);
+            CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ_generic[i], k, 32, sm));
+            if (h->occ_generic[i] < 1) return fail(POLAR_ERR_CUDA, "generic decoder cannot be resident");
+        }
+        CUDA_TRY(cudaMalloc(&h->d_prog, std::max<size_t>(1, h->prog.size()) * sizeof(uint32_t)));
+        CUDA_TRY(cudaMemcpy(h->d_prog, h->prog.data(), h->prog.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
+    const Variant* vs[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (e) {
+        vs[0] = &e->tp_f32;
+        vs[1] = &e->tp_i8;
+        vs[2] = &e->lat_f32;
+        vs[3] = &e->lat_i8;
+    }
+    for (int i = 0; i < (e ? 4 : 0); ++i) {
         const void* k = *vs[i]->kern;
         CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*vs[i]->smem));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ[i], k, (int)(vs[i]->threads * vs[i]->frames),
@@ -156,13 +180,16 @@ extern "C" polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t*
         if (kRegistry[i].hash == hsh && kRegistry[i].N == N && kRegistry[i].K == K &&
             std::memcmp(kRegistry[i].mask, m.data(), N) == 0)
             e = &kRegistry[i];
-    if (!e) return fail(POLAR_ERR_UNSUPPORTED_CODE, "no decoder was specialised for this (N=%u, K=%u) frozen set", N, K);
     polar_code* h = new polar_code;
     h->N = N;
     h->K = K;
     h->mask = std::move(m);
-    h->entry = e;
-    h->n_ops = (uint32_t)schedule(build_tree((int)N, h->mask.data())).size();
+    h->entry = e;  // nullptr: no specialised decoder, the generic (interpreted) one is used
+    const Tree tree = build_tree((int)N, h->mask.data());
+    const std::vector<std::string> ops = schedule(tree);
+    h->n_ops = (uint32_t)ops.size();
+    for (auto& o : ops) h->sched += o + ";";
+    h->prog = program(tree);  // the generic decoder serves unregistered codes and variant 3
     h->systematic_ok = superset_closed((int)N, h->mask.data());
     polar_status s = init_device(h);
     if (s != POLAR_OK) {
@@ -177,6 +204,7 @@ extern "C" void polar_code_destroy(polar_code* h) {
     if (!h) return;
     if (h->dev_ready) {
         if (h->d_trace) cudaFree(h->d_trace);
+        if (h->d_prog) cudaFree(h->d_prog);
         cudaFree(h->d_pos);
         cudaFree(h->d_info_mask);
         cudaFree(h->d_gtab);
@@ -197,13 +225,19 @@ extern "C" polar_status polar_code_query(const polar_code* h, uint32_t* N, uint3
     if (N) *N = h->N;
     if (K) *K = h->K;
     if (n_ops) *n_ops = h->n_ops;
-    if (smem_bytes) *smem_bytes = *h->entry->tp_i8.smem;
-    if (warp_root) *warp_root = h->entry->warp_root;
+    if (smem_bytes) *smem_bytes = h->entry ? *h->entry->tp_i8.smem : (uint32_t)polar_generic_smem(true, (int)h->N, (int)h->K);
+    if (warp_root) *warp_root = h->entry ? h->entry->warp_root : 0;
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_code_is_specialised(const polar_code* h, int* specialised) {
+    if (!h || !specialised) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
+    *specialised = h->entry != nullptr;
     return POLAR_OK;
 }
 
 extern "C" polar_status polar_code_set_variant(polar_code* h, int variant) {
-    if (!h || variant < 0 || variant > 2) return fail(POLAR_ERR_INVALID_ARGUMENT, "variant must be 0, 1 or 2");
+    if (!h || variant < 0 || variant > 3) return fail(POLAR_ERR_INVALID_ARGUMENT, "variant must be 0, 1, 2 or 3");
     h->variant = variant;
     return POLAR_OK;
 }
@@ -216,7 +250,7 @@ extern "C" polar_status polar_code_mask(const polar_code* h, uint8_t* mask_out) 
 
 extern "C" polar_status polar_code_schedule(const polar_code* h, char* buf, uint32_t cap, uint32_t* needed) {
     if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
-    const char* s = h->entry->schedule;
+    const char* s = h->sched.c_str();
     const uint32_t len = (uint32_t)std::strlen(s);
     if (needed) *needed = len + 1;
     if (buf && cap) {
@@ -261,6 +295,18 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     if (((uintptr_t)out & 3) != 0) return fail(POLAR_ERR_INVALID_ARGUMENT, "info_bits must be 4-byte aligned");
     if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device was available when the handle was created");
     const RegistryEntry* e = h->entry;
+    if (!e || h->variant == 3) {  // generic decoder
+        const void* kern = polar_generic_kernel(i8);
+        const int sm = polar_generic_smem(i8, (int)h->N, (int)h->K);
+        const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)h->occ_generic[i8 ? 1 : 0] * h->n_sm);
+        long long nn = (long long)n;
+        const uint32_t* gtab = h->d_gtab;
+        const uint32_t* prog = h->d_prog;
+        int nops = (int)h->prog.size(), N = (int)h->N, K = (int)h->K;
+        void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&prog, (void*)&nops, (void*)&N, (void*)&K};
+        CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(32), args, sm, s));
+        return POLAR_OK;
+    }
     // Latency variant (a CTA per frame) for batches that cannot fill the GPU with one frame
     // per warp; otherwise the throughput variant (a warp per frame).
     // (measured crossover, profiles/r1_sweeps.md: at N >= 16384 one latency wave of #SMs

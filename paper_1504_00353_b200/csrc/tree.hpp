@@ -102,6 +102,49 @@ inline std::vector<std::string> schedule(const Tree& t) {
     return ops;
 }
 
+// The same traversal as a compact program for the generic (interpreted) decoder, the GPU
+// analogue of the paper's instruction-based decoder: one uint32 per
+// op = opcode | log2(N_v) << 4 | node offset << 9.  Combine_R0 needs no instruction (the
+// right half of beta is already zero).
+enum : uint32_t { OP_F = 0, OP_G = 1, OP_G0R = 2, OP_R1 = 3, OP_REP = 4, OP_SPC = 5, OP_COMB = 6, OP_COMB0R = 7 };
+
+inline uint32_t encode_op(uint32_t op, int n, int off) {
+    int k = 0;
+    while ((1 << k) < n) ++k;
+    return op | (uint32_t)k << 4 | (uint32_t)off << 9;
+}
+
+inline void program_rec(const Tree& t, int id, std::vector<uint32_t>& p) {
+    const Node& v = t.nodes[id];
+    switch (v.kind) {
+        case Kind::Rate0: return;
+        case Kind::Rate1: p.push_back(encode_op(OP_R1, v.n, v.off)); return;
+        case Kind::Rep: p.push_back(encode_op(OP_REP, v.n, v.off)); return;
+        case Kind::Spc: p.push_back(encode_op(OP_SPC, v.n, v.off)); return;
+        case Kind::Split: break;
+    }
+    const Node& l = t.nodes[v.left];
+    const Node& r = t.nodes[v.right];
+    if (l.kind == Kind::Rate0) {
+        p.push_back(encode_op(OP_G0R, v.n, v.off));
+        program_rec(t, v.right, p);
+        p.push_back(encode_op(OP_COMB0R, v.n, v.off));
+        return;
+    }
+    p.push_back(encode_op(OP_F, v.n, v.off));
+    program_rec(t, v.left, p);
+    if (r.kind == Kind::Rate0) return;
+    p.push_back(encode_op(OP_G, v.n, v.off));
+    program_rec(t, v.right, p);
+    p.push_back(encode_op(OP_COMB, v.n, v.off));
+}
+
+inline std::vector<uint32_t> program(const Tree& t) {
+    std::vector<uint32_t> p;
+    program_rec(t, 0, p);
+    return p;
+}
+
 // Information set closed under bit-superset: i in A implies i | 2^b in A for every b.
 // Required by the two-pass systematic encoder (reading C4).
 inline bool superset_closed(int N, const uint8_t* frozen) {

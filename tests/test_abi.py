@@ -101,9 +101,11 @@ def test_create_validation():
     with pytest.raises(pb.PolarError) as e:
         pb.PolarCode(48, 32, bad)  # N not a power of two
     assert e.value.status == pb.POLAR_ERR_INVALID_ARGUMENT
-    with pytest.raises(pb.PolarError) as e:
-        pb.PolarCode(64, 32, random_mask(999, 64, 32))  # not specialised in this build
-    assert e.value.status == pb.POLAR_ERR_UNSUPPORTED_CODE
+    # a frozen set no decoder was specialised for gets the generic (interpreted) decoder
+    g = pb.PolarCode(64, 32, random_mask(999, 64, 32))
+    assert not g.specialised
+    assert g.schedule() == oracle.fastssc_trace(random_mask(999, 64, 32))
+    assert pb.PolarCode(8, 5, np.array([1, 1, 0, 0, 1, 0, 0, 0], np.uint8)).specialised
 
 
 def test_handle_roundtrip_and_query():

@@ -113,6 +113,35 @@ def test_f32_equals_plain_sc(name, N, K, mask, ebn0):
     assert_same(gpu_decode(code, llr)[keep], want[keep], name)
 
 
+GENERIC = [(2, 1, 301), (4, 2, 302), (8, 3, 303), (16, 9, 304), (32, 20, 305), (64, 30, 306), (256, 100, 307),
+           (1024, 600, 308), (4096, 3000, 309), (32768, 20000, 310)]
+
+
+@pytest.mark.parametrize("N,K,seed", GENERIC, ids=[f"{n}_{k}" for n, k, _ in GENERIC])
+def test_generic_decoder_random_masks(N, K, seed):
+    """N1: frozen sets without a specialised decoder use the interpreted decoder."""
+    from seeded_inputs import random_mask
+
+    mask = random_mask(seed, N, K)
+    code = pb.PolarCode(N, K, mask)
+    assert not code.specialised
+    n = 2 if N >= 32768 else 24 if N >= 4096 else 200
+    cases = {"i8": random_llr_i8(seed, (n, N), -128, 127), "i8_ties": random_llr_i8(seed + 1, (n, N), -2, 2),
+             "f32": random_llr_f32(seed, (n, N), 3.0), "f32_ints": random_llr_f32(seed + 2, (n, N), 1.0).round()}
+    for what, x in cases.items():
+        assert_same(gpu_decode(code, x.astype(x.dtype)), expected(mask, x), f"generic ({N},{K}) {what}")
+
+
+@pytest.mark.parametrize("name,N,K,mask,ebn0", [c for c in CODES if c[1] in (8, 1024, 2048, 32768)],
+                         ids=[c[0] for c in CODES if c[1] in (8, 1024, 2048, 32768)])
+def test_generic_variant_equals_oracle_on_registered_codes(name, N, K, mask, ebn0):
+    code = pb.PolarCode(N, K, mask)
+    code.set_variant("generic")
+    _, llr, q = frames(mask, K, 8 if N >= 32768 else 100, ebn0 - 1.0, seed=55)
+    for x in (llr, q):
+        assert_same(gpu_decode(code, x), expected(mask, x), f"{name} generic {x.dtype}")
+
+
 def test_ragged_batches_and_grid_striding():
     """Frame counts that are not multiples of the CTA's frames and exceed one resident wave."""
     for (N, K, e) in [(64, 32, 2.0), (1024, 512, 2.5), (4096, 2048, 2.5)]:

@@ -112,9 +112,42 @@ def batch(a):
               flush=True)
 
 
+def idud(a):
+    """Instruction-based (generic, interpreted) vs unrolled (specialised) decoder on the same
+    code -- the GPU analogue of the paper's tab:impl:tp:algo-unroll."""
+    N, K = map(int, a.code.split(","))
+    code = pb.PolarCode.ga(N, K, a.design)
+    W = code.info_words
+    s = torch.cuda.current_stream()
+    for batch in (1, a.batch):
+        llr = torch.empty(batch, N, dtype=torch.int8, device="cuda")
+        code.gen_bpsk_awgn(SEED, 0, batch, a.design, 4.0, llr_i8=llr)
+        out = torch.empty(batch, W, dtype=torch.int32, device="cuda")
+        ref = None
+        for variant in ("auto", "generic"):
+            code.set_variant(variant)
+            for _ in range(3):
+                code.decode_i8(llr, out)
+            reps = 50 if batch == 1 else 5
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(reps):
+                code.decode_i8(llr, out)
+            e1.record(s)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            if ref is None:
+                ref = out.clone()
+            assert torch.equal(out, ref), "generic and unrolled decoders disagree"
+            print(json.dumps({"code": [N, K], "decoder": "unrolled" if variant == "auto" else "instruction-based",
+                              "batch": batch, "us": ms * 1e3, "info_gbps": batch * K / (ms * 1e-3) / 1e9}), flush=True)
+    code.set_variant("auto")
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["fer", "batch"])
+    ap.add_argument("mode", choices=["fer", "batch", "idud"])
+    ap.add_argument("--batch", type=int, default=65536)
     ap.add_argument("--code", default="32768,27568")
     ap.add_argument("--design", type=float, default=4.0)
     ap.add_argument("--points", default="3.5,3.75,4.0,4.25")
@@ -125,4 +158,4 @@ if __name__ == "__main__":
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--max-log4", type=int, default=8)
     a = ap.parse_args()
-    (fer if a.mode == "fer" else batch)(a)
+    {"fer": fer, "batch": batch, "idud": idud}[a.mode](a)
