@@ -46,6 +46,8 @@ struct Spec {
     int fpc_max = 16;  // most lockstep frames (warps) per CTA in the throughput variant
     std::set<int> dedup;  // sizes of subtrees shared as noinline functions (DEDUP=16,32,..)
     int ll = 0;           // lane-local tiny subtrees up to this size (LL=8 enables; measured slower, profiles/r1_history.md)
+    int cps = 1;          // throughput variant: CTAs per SM requested from ptxas (__launch_bounds__ min blocks)
+    bool gbeta = false;   // throughput variant: decision bits in the global slot scratch too (GBETA=1)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
 };
 
@@ -335,10 +337,25 @@ struct CtaEmitter {
         body << "        if constexpr (WF32) { " << subst("wst") << " } else { " << subst(slot) << " }\n";
     }
 
+    // The warp subtree is emitted twice when small subtrees are shared (DEDUP): with the
+    // shared noinline functions for the throughput variant (smaller code, measured +11% at
+    // N = 32768) and fully inlined for the latency variant (the calls cost ~6 us of batch-1
+    // latency), profiles/r1_history.md.
+    SharedFns* sh_lat = nullptr;
     void sub_call(int id, const std::string& src) {
         std::string fname = "sub" + std::to_string(n_subs++);
-        emit_warp_sub(subs, t, id, fname, sh);
-        emit("if (gtid<T>() < 32) " + fname + "<P>(" + src + ", beta);");
+        if (sh && !sh->sizes.empty() && sh_lat) {
+            TraceMarks* keep = g_marks;
+            g_marks = nullptr;  // trace marks only in the latency copy
+            emit_warp_sub(subs, t, id, fname + "_tp", sh);
+            g_marks = keep;
+            emit_warp_sub(subs, t, id, fname + "_lat", sh_lat);
+            emit("if constexpr (T == 32) { " + fname + "_tp<P>(" + src + ", beta); } else { if (gtid<T>() < 32) " +
+                 fname + "_lat<P>(" + src + ", beta); }");
+        } else {
+            emit_warp_sub(subs, t, id, fname, sh);
+            emit("if (gtid<T>() < 32) " + fname + "<P>(" + src + ", beta);");
+        }
         emit("sync();");
     }
 
@@ -432,7 +449,8 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
       << "    static constexpr int W = " << W << ";\n";
     if (!cta_phase) {
         o << "    static constexpr int STAGE_ELEMS = 0;\n    static constexpr int STAGE_ELEMS_SMEM = 0;\n"
-          << "    static constexpr int GSTAGE_ELEMS = 0;\n    static constexpr int WST = 0;\n";
+          << "    static constexpr int GSTAGE_ELEMS = 0;\n    static constexpr int WST = 0;\n"
+          << "    static constexpr bool GBETA = false;\n";
         emit_warp_sub(o, t, 0, "decode_root", &sh);
         o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, typename P::st_t*, typename P::v_t*,\n"
@@ -441,6 +459,8 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     } else {
         std::ostringstream body, subs;
         CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, {}, {}, 0, &sh};
+        SharedFns sh_none{sp.mask, {}, {}, {}};
+        ce.sh_lat = &sh_none;
         int acc = 0, sacc = 0, gacc = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         for (int m = sp.N / 2; m >= W; m /= 2) {
@@ -458,7 +478,8 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         o << "    static constexpr int STAGE_ELEMS = " << acc << ";\n"
           << "    static constexpr int STAGE_ELEMS_SMEM = " << sacc << ";  // GTOP layout\n"
           << "    static constexpr int GSTAGE_ELEMS = " << gacc << ";\n"
-          << "    static constexpr int WST = " << W << ";  // f32 stage feeding the register subtrees\n";
+          << "    static constexpr int WST = " << W << ";  // f32 stage feeding the register subtrees\n"
+          << "    static constexpr bool GBETA = " << (sp.gbeta && gacc > 0 ? "true" : "false") << ";\n";
         o << subs.str();
         o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
@@ -487,6 +508,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         bool chan_smem;
         int fpc;
         bool gtop;
+        int minb;
     };
     auto bytes = [&](const char* prof) { return sp.N * (std::string(prof) == "PF32" ? 4 : 1); };
     // Throughput variant: as many lockstep warps (frames) per CTA as the shared memory of one
@@ -502,24 +524,26 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         const int s = std::string(prof) == "PF32" ? 4 : 1;
         const int stages = a16(std::max(0, cta_phase ? sp.N - W - g_elems : 0) * s);
         const int outw = a16((sp.K + 31) / 32 * 4);
-        const int per = (chan_smem ? 2 * a16(sp.N * s) : 0) + stages + a16(std::max(1, sp.N / 32) * 4) +
+        const bool gb = sp.gbeta && g_elems > 0;
+        const int per = (chan_smem ? 2 * a16(sp.N * s) : 0) + stages + (gb ? 0 : a16(std::max(1, sp.N / 32) * 4)) +
                         (stages >= outw ? 0 : outw) + 16;
         return std::max(1, std::min(sp.fpc_max, (220 * 1024) / per));
     };
     const bool cs_f = 2 * bytes("PF32") <= 16384, cs_i = 2 * bytes("PI8") <= 16384;
     const bool gt = g_elems > 0;
     std::vector<V> vars = {
-        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f), gt},
-        {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i), gt},
-        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1, false},
-        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1, false},
+        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f), gt, 1},
+        {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i), gt, sp.cps},
+        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1, false, 1},
+        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1, false, 1},
     };
     for (auto& v : vars) {
         const std::string targs = std::string("pd::") + v.prof + ", " + C + ", " + std::to_string(v.T) + ", " +
                                   std::to_string(v.fpc) + ", " + (v.chan_smem ? "true" : "false") + ", " +
                                   (v.gtop ? "true" : "false");
+        const std::string kargs = targs + ", " + std::to_string(v.minb);
         o << "extern const void* const polar_kern_" << sp.name << "_" << v.tag << " = (const void*)&pd::k_frame<"
-          << targs << ">;\n"
+          << kargs << ">;\n"
           << "extern const unsigned polar_smem_" << sp.name << "_" << v.tag << " = pd::FrameLayout<" << targs
           << ">::SMEM;\n";
         reg_decl << "extern const void* const polar_kern_" << sp.name << "_" << v.tag << ";\n"
@@ -542,7 +566,10 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     for (auto& v : vars)
         reg_entries << ", {&polar_kern_" << sp.name << "_" << v.tag << ", &polar_smem_" << sp.name << "_" << v.tag
                     << ", " << v.T << ", " << v.fpc << ", "
-                    << (v.gtop ? g_elems * (std::string(v.prof) == "PF32" ? 4 : 1) : 0) << "}";
+                    << (v.gtop ? a16(g_elems * (std::string(v.prof) == "PF32" ? 4 : 1)) +
+                                     (sp.gbeta ? a16(std::max(1, sp.N / 32) * 4) : 0)
+                               : 0)
+                    << "}";
     reg_entries << ", \"" << sched << "\"},\n";
 }
 
@@ -600,6 +627,8 @@ int main(int argc, char** argv) {
             else if (opt.rfind("FPC=", 0) == 0) sp.fpc_max = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("GS=", 0) == 0) sp.gs = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("LL=", 0) == 0) sp.ll = std::atoi(opt.c_str() + 3);
+            else if (opt.rfind("CPS=", 0) == 0) sp.cps = std::atoi(opt.c_str() + 4);
+            else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();
                 std::stringstream ds(opt.substr(6));

@@ -60,7 +60,12 @@ struct FrameLayout {
     static constexpr bool WF32 = T > 32;
     static constexpr int WST_OFF = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t));
     static constexpr int STAGES = WST_OFF + (WF32 ? align16(C::WST * (int)sizeof(typename P::v_t)) : 0);
-    static constexpr int BETA = align16((C::N >= 32 ? C::N / 32 : 1) * 4);
+    // GTOP && C::GBETA: the decision bits also live in the frame slot's global scratch
+    static constexpr bool GB = GTOP && C::GBETA;
+    static constexpr int BETA_BYTES = align16((C::N >= 32 ? C::N / 32 : 1) * 4);
+    static constexpr int BETA = GB ? 0 : BETA_BYTES;
+    static constexpr int GSTAGE_BYTES = align16(C::GSTAGE_ELEMS * (int)sizeof(st_t));
+    static constexpr int GSLOT = GSTAGE_BYTES + (GB ? BETA_BYTES : 0);  // global bytes per slot
     // output staging words: the stage area is free after the decode when it is large enough
     static constexpr int OUTW = align16((C::K + 31) / 32 * 4);
     static constexpr int STG = STAGES >= OUTW ? 0 : OUTW;
@@ -71,8 +76,8 @@ struct FrameLayout {
 // FPC frame groups of T threads per CTA (FPC > 1 only with T = 32).
 // GTOP: the largest stages (N/2 and N/4 by default) live in global scratch (L2-resident), one slot per frame
 // group of the persistent grid, so that more frames fit in shared memory per SM.
-template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP>
-__global__ void __launch_bounds__(T * FPC)
+template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP, int MINB = 1>
+__global__ void __launch_bounds__(T * FPC, MINB)
     k_frame(const void* __restrict__ llr_, long long n_frames, uint32_t* __restrict__ out,
             const uint32_t* __restrict__ gtab, void* __restrict__ gscratch) {
     static_assert(FPC == 1 || T == 32, "");
@@ -90,11 +95,12 @@ __global__ void __launch_bounds__(T * FPC)
     in_t* const buf1 = (in_t*)(smem + (DBL ? L::BUF : 0));
     st_t* const stages = (st_t*)(smem + L::NBUF * L::BUF);
     typename P::v_t* const wst = (typename P::v_t*)(smem + L::NBUF * L::BUF + L::WST_OFF);
-    uint32_t* const beta = (uint32_t*)(smem + L::NBUF * L::BUF + L::STAGES);
+    unsigned char* const gslot = GTOP ? (unsigned char*)gscratch + ((long long)blockIdx.x * FPC + grp) * L::GSLOT : nullptr;
+    uint32_t* const beta = L::GB ? (uint32_t*)(gslot + L::GSTAGE_BYTES) : (uint32_t*)(smem + L::NBUF * L::BUF + L::STAGES);
     uint32_t* const stg = (uint32_t*)(L::STG ? smem + L::NBUF * L::BUF + L::STAGES + L::BETA : (unsigned char*)stages);
     uint64_t* const bar = (uint64_t*)(smem + L::NBUF * L::BUF + L::STAGES + L::BETA + L::STG);
     const in_t* llr = (const in_t*)llr_;
-    st_t* const gst = GTOP ? (st_t*)gscratch + ((long long)blockIdx.x * FPC + grp) * C::GSTAGE_ELEMS : nullptr;
+    st_t* const gst = (st_t*)gslot;
     const unsigned tid = FPC > 1 ? (threadIdx.x & 31u) : threadIdx.x;  // thread index in its group
     const bool leader = tid == 0;
 
