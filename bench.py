@@ -47,7 +47,7 @@ def _dist():
 
 class Clocks:
     """Samples SM clocks and throttle reasons during the timed region: NVML in-process every
-    5 ms (the timed region is tens of ms), nvidia-smi as a fallback."""
+    1 ms (the timed region is tens of ms), nvidia-smi as a fallback."""
 
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
@@ -75,7 +75,7 @@ class Clocks:
                 self.rows.append((float(sm), float(self._max), [bool(r & m) for m in self._masks]))
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.001)
 
     def _read_smi(self):
         for line in self._p.stdout:
