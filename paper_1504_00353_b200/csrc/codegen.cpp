@@ -266,13 +266,14 @@ std::string Emitter::shared_fn(int id) {
 }
 
 // A warp subtree function: root node id, whose input LLRs are at `src` (shared memory).
-void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::string& fname, SharedFns* sh) {
+void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::string& fname, SharedFns* sh,
+                   bool chan = false) {
     const Node& v = t.nodes[id];
     const int R = v.n;
     o << "    template <class P, class SrcT>\n"
       << "    static PD_INLINE void " << fname << "(const SrcT* src_ptr, uint32_t* beta) {\n"
       << "        using V = typename P::v_t;\n"
-      << "        const MemSrc<P, SrcT> src{src_ptr};\n";
+      << "        const MemSrc<P, SrcT, " << (chan ? "true" : "false") << "> src{src_ptr};\n";
     for (int k = ilog2(R) - 1; k >= 0; --k) {
         const int size = 1 << k;
         o << "        V r" << k << "[" << (size >= 32 ? size / 32 : 1) << "];\n";
@@ -451,7 +452,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         o << "    static constexpr int STAGE_ELEMS = 0;\n    static constexpr int STAGE_ELEMS_SMEM = 0;\n"
           << "    static constexpr int GSTAGE_ELEMS = 0;\n    static constexpr int WST = 0;\n"
           << "    static constexpr bool GBETA = false;\n";
-        emit_warp_sub(o, t, 0, "decode_root", &sh);
+        emit_warp_sub(o, t, 0, "decode_root", &sh, true);  // reads the channel
         o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, typename P::st_t*, typename P::v_t*,\n"
           << "                                 uint32_t* beta, const SyncT&) {\n"

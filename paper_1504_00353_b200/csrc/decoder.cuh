@@ -362,16 +362,22 @@ struct RegSrc {
     }
 };
 
-template <class P, class T>
+// CHAN: the source is the channel (int8 input -128 is clamped, reading C8); stages written by
+// the decoder never hold -128, so their loads skip the clamp.
+template <class P, class T, bool CHAN = true>
 struct MemSrc {
     using V = typename P::v_t;
     const T* p;
-    PD_INLINE V v(int j) const { return P::ld(p[lane_id() + 32 * j]); }
-    PD_INLINE V one(int n) const { return P::ld(p[lane_id() & (n - 1)]); }
+    PD_INLINE V ld(T x) const {
+        if constexpr (!CHAN && sizeof(T) == 1) return __int_as_float(0x4B400000 + (int)x) - 12582912.0f;
+        else return P::ld(x);
+    }
+    PD_INLINE V v(int j) const { return ld(p[lane_id() + 32 * j]); }
+    PD_INLINE V one(int n) const { return ld(p[lane_id() & (n - 1)]); }
     PD_INLINE void pair(int h, V& x, V& y) const {
         const unsigned l = lane_id() & (2 * h - 1);
-        x = P::ld(p[l]);
-        y = P::ld(p[l ^ h]);
+        x = ld(p[l]);
+        y = ld(p[l ^ h]);
     }
 };
 
