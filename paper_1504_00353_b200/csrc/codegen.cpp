@@ -47,6 +47,7 @@ struct Spec {
     std::set<int> dedup;  // sizes of subtrees shared as noinline functions (DEDUP=16,32,..)
     int ll = 0;           // lane-local tiny subtrees up to this size (LL=8 enables; measured slower, profiles/r1_history.md)
     int cps = 1;          // throughput variant: CTAs per SM requested from ptxas (__launch_bounds__ min blocks)
+    int wlat = 0;         // latency variant's warp-subtree size (WLAT=; default W)
     bool gbeta = false;   // throughput variant: decision bits in the global slot scratch too (GBETA=1)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
 };
@@ -437,14 +438,18 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     std::vector<std::string> ops = schedule(t);
     const int W = std::min(sp.N, sp.W);
     const bool cta_phase = sp.N > W;
-    const int t_lat = cta_phase ? sp.T : 32;
     SharedFns sh{sp.mask, sp.dedup, {}, {}};
     TraceMarks marks;
     g_marks = &marks;
     g_ll = sp.ll;
     marks.mark("start");
     std::ostringstream o;
-    o << "struct Code {\n"
+    // One struct per warp-subtree size: "Code" (throughput variants) and, when WLAT differs,
+    // "CodeLat" (latency variants).
+    auto emit_struct = [&](const std::string& sname, int Wv) {
+    const int W = Wv;
+    const bool cta_phase = sp.N > W;
+    o << "struct " << sname << " {\n"
       << "    static constexpr int N = " << sp.N << ";\n"
       << "    static constexpr int K = " << sp.K << ";\n"
       << "    static constexpr int W = " << W << ";\n";
@@ -489,7 +494,19 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
           << "        PTRACE(0);\n"
           << body.str() << "    }\n";
     }
-    o << "};\n\n}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
+    o << "};\n\n";
+    };
+    const int WL = std::min(sp.N, sp.wlat > 0 ? sp.wlat : W);
+    const bool two = WL != W;
+    if (two) {
+        g_marks = nullptr;  // trace marks belong to the latency variant's code
+        emit_struct("Code", W);
+        g_marks = &marks;
+        emit_struct("CodeLat", WL);
+    } else {
+        emit_struct("Code", W);
+    }
+    o << "}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
     {
         std::ostringstream head;
         head << "// Generated by codegen.cpp for code " << sp.name << " (N=" << sp.N << ", K=" << sp.K << ", "
@@ -502,6 +519,8 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         o << head.str() << rest;
     }
     const std::string C = "pd::code_" + sp.name + "::Code";
+    const std::string CL = "pd::code_" + sp.name + (two ? "::CodeLat" : "::Code");
+    const int t_lat = sp.N > WL ? sp.T : 32;
     struct V {
         const char* tag;
         const char* prof;
@@ -510,6 +529,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         int fpc;
         bool gtop;
         int minb;
+        bool lat;
     };
     auto bytes = [&](const char* prof) { return sp.N * (std::string(prof) == "PF32" ? 4 : 1); };
     // Throughput variant: as many lockstep warps (frames) per CTA as the shared memory of one
@@ -533,13 +553,13 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     const bool cs_f = 2 * bytes("PF32") <= 16384, cs_i = 2 * bytes("PI8") <= 16384;
     const bool gt = g_elems > 0;
     std::vector<V> vars = {
-        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f), gt, 1},
-        {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i), gt, sp.cps},
-        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1, false, 1},
-        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1, false, 1},
+        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f), gt, 1, false},
+        {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i), gt, sp.cps, false},
+        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1, false, 1, true},
+        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1, false, 1, true},
     };
     for (auto& v : vars) {
-        const std::string targs = std::string("pd::") + v.prof + ", " + C + ", " + std::to_string(v.T) + ", " +
+        const std::string targs = std::string("pd::") + v.prof + ", " + (v.lat ? CL : C) + ", " + std::to_string(v.T) + ", " +
                                   std::to_string(v.fpc) + ", " + (v.chan_smem ? "true" : "false") + ", " +
                                   (v.gtop ? "true" : "false");
         const std::string kargs = targs + ", " + std::to_string(v.minb);
@@ -629,6 +649,7 @@ int main(int argc, char** argv) {
             else if (opt.rfind("GS=", 0) == 0) sp.gs = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("LL=", 0) == 0) sp.ll = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("CPS=", 0) == 0) sp.cps = std::atoi(opt.c_str() + 4);
+            else if (opt.rfind("WLAT=", 0) == 0) sp.wlat = std::atoi(opt.c_str() + 5);
             else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();
