@@ -48,6 +48,7 @@ struct Spec {
     int ll = 0;           // lane-local tiny subtrees up to this size (LL=8 enables; measured slower, profiles/r1_history.md)
     int cps = 1;          // throughput variant: CTAs per SM requested from ptxas (__launch_bounds__ min blocks)
     int wlat = 0;         // latency variant's warp-subtree size (WLAT=; default W)
+    int xw = 0;           // latency variant: CTA-level nodes up to XW run on warp 0 alone (XW=)
     bool gbeta = false;   // throughput variant: decision bits in the global slot scratch too (GBETA=1)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
 };
@@ -312,8 +313,21 @@ struct CtaEmitter {
     // Emit one statement; "@W" (the stage of size W) becomes `wst` under WF32, else its slot
     // in the stage arrays.
     std::string last_op;
-    void emit(const std::string& stmt) {
-        if (stmt == "sync();" && g_marks) {
+    // Warp-0 regions (latency variant, XW): a CTA-level node of size <= XW is decoded by warp 0
+    // alone -- stage loops with 32 threads, __syncwarp instead of CTA barriers -- and the other
+    // warps wait at one barrier after the region.  In the throughput variant (T = 32) the
+    // rewrite is the identity.
+    int XW = 0;
+    bool in_region = false;
+    static std::string region(std::string x) {
+        for (size_t q; (q = x.find("<P, T, ")) != std::string::npos;) x.replace(q, 7, "<P, 32, ");
+        for (size_t q; (q = x.find("<T, ")) != std::string::npos;) x.replace(q, 4, "<32, ");
+        if (x == "sync();") x = "__syncwarp();";
+        return x;
+    }
+    void emit(const std::string& stmt0) {
+        const std::string stmt = in_region ? region(stmt0) : stmt0;
+        if ((stmt == "sync();" || stmt == "__syncwarp();") && g_marks) {
             emit_raw(stmt);
             std::string lab = last_op.rfind("if (gtid", 0) == 0 ? std::string("subtree") : last_op.substr(0, last_op.find('('));
             emit_raw(g_marks->mark("cta:" + lab));
@@ -371,6 +385,15 @@ struct CtaEmitter {
     void child(int id, const std::string& src) {
         const Node& v = t.nodes[id];
         if (v.kind == Kind::Rate0) return;  // beta zeroed at frame start
+        if (v.n > W && v.n <= XW && !in_region) {
+            emit_raw("if (gtid<T>() < 32) {  // warp-0 region");
+            in_region = true;
+            cta(id, src);
+            in_region = false;
+            emit_raw("}");
+            emit("sync();");
+            return;
+        }
         if (v.n > W) cta(id, src);
         else sub_call(id, src);
     }
@@ -467,6 +490,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         CtaEmitter ce{t, body, subs, W, sp.T, sp.N, {}, {}, {}, 0, &sh};
         SharedFns sh_none{sp.mask, {}, {}, {}};
         ce.sh_lat = &sh_none;
+        ce.XW = sp.xw;
         int acc = 0, sacc = 0, gacc = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         for (int m = sp.N / 2; m >= W; m /= 2) {
@@ -650,6 +674,7 @@ int main(int argc, char** argv) {
             else if (opt.rfind("LL=", 0) == 0) sp.ll = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("CPS=", 0) == 0) sp.cps = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("WLAT=", 0) == 0) sp.wlat = std::atoi(opt.c_str() + 5);
+            else if (opt.rfind("XW=", 0) == 0) sp.xw = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();
