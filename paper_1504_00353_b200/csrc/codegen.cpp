@@ -49,6 +49,7 @@ struct Spec {
     int cps = 1;          // throughput variant: CTAs per SM requested from ptxas (__launch_bounds__ min blocks)
     int wlat = 0;         // latency variant's warp-subtree size (WLAT=; default W)
     int xw = 0;           // latency variant: CTA-level nodes up to XW run on warp 0 alone (XW=)
+    bool helper = false;  // latency variant: instruction run-ahead helper warp (HELPER=1)
     bool gbeta = false;   // throughput variant: decision bits in the global slot scratch too (GBETA=1)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
 };
@@ -269,11 +270,12 @@ std::string Emitter::shared_fn(int id) {
 
 // A warp subtree function: root node id, whose input LLRs are at `src` (shared memory).
 void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::string& fname, SharedFns* sh,
-                   bool chan = false) {
+                   bool chan = false, bool noinline = false) {
     const Node& v = t.nodes[id];
     const int R = v.n;
     o << "    template <class P, class SrcT>\n"
-      << "    static PD_INLINE void " << fname << "(const SrcT* src_ptr, uint32_t* beta) {\n"
+      << "    static " << (noinline ? "__device__ __noinline__" : "PD_INLINE") << " void " << fname
+      << "(const SrcT* src_ptr, uint32_t* beta) {\n"
       << "        using V = typename P::v_t;\n"
       << "        const MemSrc<P, SrcT, " << (chan ? "true" : "false") << "> src{src_ptr};\n";
     for (int k = ilog2(R) - 1; k >= 0; --k) {
@@ -358,14 +360,17 @@ struct CtaEmitter {
     // N = 32768) and fully inlined for the latency variant (the calls cost ~6 us of batch-1
     // latency), profiles/r1_history.md.
     SharedFns* sh_lat = nullptr;
+    bool helper = false;                  // HELPER: instruction run-ahead warp (latency variant)
+    std::vector<std::string> lat_subs;    // latency-copy subtree functions, in call order
     void sub_call(int id, const std::string& src) {
         std::string fname = "sub" + std::to_string(n_subs++);
-        if (sh && !sh->sizes.empty() && sh_lat) {
+        if ((sh && !sh->sizes.empty() && sh_lat) || helper) {
             TraceMarks* keep = g_marks;
             g_marks = nullptr;  // trace marks only in the latency copy
             emit_warp_sub(subs, t, id, fname + "_tp", sh);
             g_marks = keep;
-            emit_warp_sub(subs, t, id, fname + "_lat", sh_lat);
+            emit_warp_sub(subs, t, id, fname + "_lat", sh_lat ? sh_lat : sh, false, helper);
+            lat_subs.push_back(fname + "_lat");
             emit("if constexpr (T == 32) { " + fname + "_tp<P>(" + src + ", beta); } else { if (gtid<T>() < 32) " +
                  fname + "_lat<P>(" + src + ", beta); }");
         } else {
@@ -427,7 +432,9 @@ struct CtaEmitter {
         const std::string D = stage(h);
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
+        // HELPER: one arrive per subtree call, just before the stage op that produces its input
         if (l.kind == Kind::Rate0) {
+            if (helper && h == W && r.kind != Kind::Rate0) emit("if (gtid<T>() < 32) sync.helper_arrive();");
             emit("cG0R<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
             emit("sync();");
             if (id == 0) emit("sync.root_g_done();");
@@ -436,10 +443,12 @@ struct CtaEmitter {
             emit("sync();");
             return;
         }
+        if (helper && h == W) emit("if (gtid<T>() < 32) sync.helper_arrive();");
         emit("cF<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
         emit("sync();");
         child(v.left, D);
         if (r.kind == Kind::Rate0) return;
+        if (helper && h == W) emit("if (gtid<T>() < 32) sync.helper_arrive();");
         emit("cG<P, T, " + N_ + ", " + CL + ", false, " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ", " + B + ");");
         emit("sync();");
         if (id == 0) emit("sync.root_g_done();");
@@ -479,7 +488,9 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     if (!cta_phase) {
         o << "    static constexpr int STAGE_ELEMS = 0;\n    static constexpr int STAGE_ELEMS_SMEM = 0;\n"
           << "    static constexpr int GSTAGE_ELEMS = 0;\n    static constexpr int WST = 0;\n"
-          << "    static constexpr bool GBETA = false;\n";
+          << "    static constexpr bool GBETA = false;\n    static constexpr bool HELPER = false;\n"
+          << "    template <class P, class SyncT>\n"
+          << "    static PD_INLINE void helper(const float*, uint32_t*, const SyncT&) {}\n";
         emit_warp_sub(o, t, 0, "decode_root", &sh, true);  // reads the channel
         o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, typename P::st_t*, typename P::v_t*,\n"
@@ -491,6 +502,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         SharedFns sh_none{sp.mask, {}, {}, {}};
         ce.sh_lat = &sh_none;
         ce.XW = sp.xw;
+        ce.helper = sp.helper;
         int acc = 0, sacc = 0, gacc = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         for (int m = sp.N / 2; m >= W; m /= 2) {
@@ -509,8 +521,15 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
           << "    static constexpr int STAGE_ELEMS_SMEM = " << sacc << ";  // GTOP layout\n"
           << "    static constexpr int GSTAGE_ELEMS = " << gacc << ";\n"
           << "    static constexpr int WST = " << W << ";  // f32 stage feeding the register subtrees\n"
-          << "    static constexpr bool GBETA = " << (sp.gbeta && gacc > 0 ? "true" : "false") << ";\n";
+          << "    static constexpr bool GBETA = " << (sp.gbeta && gacc > 0 ? "true" : "false") << ";\n"
+          << "    static constexpr bool HELPER = " << (ce.helper ? "true" : "false") << ";\n";
         o << subs.str();
+        // the helper warp's run-ahead sequence: the latency copies of the subtrees, in call order
+        o << "    template <class P, class SyncT>\n"
+          << "    static PD_INLINE void helper(const float* dsrc, uint32_t* dbeta, const SyncT& sync) {\n";
+        if (ce.helper)
+            for (auto& f : ce.lat_subs) o << "        sync.helper_wait();\n        " << f << "<P>(dsrc, dbeta);\n";
+        o << "    }\n";
         o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
           << "                                 typename P::v_t* wst, uint32_t* beta, const SyncT& sync) {\n"
@@ -614,7 +633,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                     << (v.gtop ? a16(g_elems * (std::string(v.prof) == "PF32" ? 4 : 1)) +
                                      (sp.gbeta ? a16(std::max(1, sp.N / 32) * 4) : 0)
                                : 0)
-                    << "}";
+                    << ", " << (v.lat && sp.helper && sp.N > WL ? 32 : 0) << "}";
     reg_entries << ", \"" << sched << "\"},\n";
 }
 
@@ -675,6 +694,7 @@ int main(int argc, char** argv) {
             else if (opt.rfind("CPS=", 0) == 0) sp.cps = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("WLAT=", 0) == 0) sp.wlat = std::atoi(opt.c_str() + 5);
             else if (opt.rfind("XW=", 0) == 0) sp.xw = std::atoi(opt.c_str() + 3);
+            else if (opt.rfind("HELPER=", 0) == 0) sp.helper = std::atoi(opt.c_str() + 7) != 0;
             else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();

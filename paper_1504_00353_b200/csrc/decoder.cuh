@@ -335,11 +335,13 @@ __host__ __device__ constexpr int chunk_elems() {
     else return (half / T >= 16) ? 16 : (half / T >= 8) ? 8 : 4;
 }
 
-// Barrier of a T-thread frame group (a lone warp needs only __syncwarp).
+// Barrier of a T-thread frame group (a lone warp needs only __syncwarp).  A CTA-wide group
+// uses named barrier 1 over its T threads, so that an extra helper warp of the latency
+// variant (kernels.cuh) never takes part.
 template <int T>
 PD_INLINE void group_sync() {
     if constexpr (T == 32) __syncwarp();
-    else __syncthreads();
+    else asm volatile("bar.sync 1, %0;" ::"n"(T) : "memory");
 }
 
 // ------------------------------------------------------------------- warp-scope sources
@@ -748,7 +750,7 @@ PD_INLINE void cRep(const TS* __restrict__ src, TSc* scratch, uint32_t* beta) {
         } else {
             __shared__ A red[T / 32];
             if (lane_id() == 0) red[gtid<T>() >> 5] = s;
-            __syncthreads();
+            group_sync<T>();
             A tot = lane_id() < T / 32 ? red[lane_id()] : A(0);  // exact: integer-valued, |sum| < 2^24
 #pragma unroll
             for (int o = 16; o; o >>= 1) tot = P::add(tot, __shfl_xor_sync(FULL, tot, o));
@@ -798,7 +800,7 @@ PD_INLINE void cSPC(const TS* __restrict__ src, uint32_t* beta) {
             red[warp] = best;
             par[warp] = p;
         }
-        __syncthreads();
+        group_sync<T>();
         best = lane_id() < T / 32 ? red[lane_id()] : ~0ull;
 #pragma unroll
         for (int o = 16; o; o >>= 1) {

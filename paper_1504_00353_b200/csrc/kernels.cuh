@@ -38,11 +38,21 @@ struct OpSync {
     const void* next;     // next frame's channel LLRs (nullptr: none / not prefetched)
     uint32_t next_bytes;
     PD_INLINE void operator()() const {
-        if constexpr (T > 32) __syncthreads();
+        if constexpr (T > 32) asm volatile("bar.sync 1, %0;" ::"n"(T) : "memory");
         else asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
     }
     PD_INLINE void root_g_done() const {
         if (next && (threadIdx.x & (T - 1)) == 0) prefetch_l2(next, next_bytes);
+    }
+    // Instruction run-ahead (latency variant, Code::HELPER): warp 0 signals (barrier 2, 64
+    // threads) just before the stage op that feeds its next register subtree; the helper warp
+    // waits on it and then runs that subtree's (shared, non-inlined) code on dummy data about
+    // one stage op ahead of warp 0, so warp 0 finds the instructions in the SM's caches.
+    PD_INLINE void helper_arrive() const {
+        if constexpr (T > 32) asm volatile("bar.arrive 2, 64;" ::: "memory");
+    }
+    PD_INLINE void helper_wait() const {
+        if constexpr (T > 32) asm volatile("bar.sync 2, 64;" ::: "memory");
     }
 };
 
@@ -60,6 +70,10 @@ struct FrameLayout {
     static constexpr bool WF32 = T > 32;
     static constexpr int WST_OFF = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t));
     static constexpr int STAGES = WST_OFF + (WF32 ? align16(C::WST * (int)sizeof(typename P::v_t)) : 0);
+    // helper warp (latency variant, Code::HELPER): dummy subtree input and decision bits
+    static constexpr bool HELP = WF32 && C::HELPER;
+    static constexpr int HSRC = HELP ? align16(C::WST * 4) : 0;
+    static constexpr int HBETA = HELP ? align16((C::N >= 32 ? C::N / 32 : 1) * 4) : 0;
     // GTOP && C::GBETA: the decision bits also live in the frame slot's global scratch
     static constexpr bool GB = GTOP && C::GBETA;
     static constexpr int BETA_BYTES = align16((C::N >= 32 ? C::N / 32 : 1) * 4);
@@ -69,7 +83,7 @@ struct FrameLayout {
     // output staging words: the stage area is free after the decode when it is large enough
     static constexpr int OUTW = align16((C::K + 31) / 32 * 4);
     static constexpr int STG = STAGES >= OUTW ? 0 : OUTW;
-    static constexpr int PER_FRAME = NBUF * BUF + STAGES + BETA + STG + 16;
+    static constexpr int PER_FRAME = NBUF * BUF + STAGES + BETA + STG + 16 + HSRC + HBETA;
     static constexpr int SMEM = FPC * PER_FRAME;
 };
 
@@ -77,7 +91,7 @@ struct FrameLayout {
 // GTOP: the largest stages (N/2 and N/4 by default) live in global scratch (L2-resident), one slot per frame
 // group of the persistent grid, so that more frames fit in shared memory per SM.
 template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP, int MINB = 1>
-__global__ void __launch_bounds__(T * FPC, MINB)
+__global__ void __launch_bounds__(T * FPC + (T > 32 && C::HELPER ? 32 : 0), MINB)
     k_frame(const void* __restrict__ llr_, long long n_frames, uint32_t* __restrict__ out,
             const uint32_t* __restrict__ gtab, void* __restrict__ gscratch) {
     static_assert(FPC == 1 || T == 32, "");
@@ -99,6 +113,8 @@ __global__ void __launch_bounds__(T * FPC, MINB)
     uint32_t* const beta = L::GB ? (uint32_t*)(gslot + L::GSTAGE_BYTES) : (uint32_t*)(smem + L::NBUF * L::BUF + L::STAGES);
     uint32_t* const stg = (uint32_t*)(L::STG ? smem + L::NBUF * L::BUF + L::STAGES + L::BETA : (unsigned char*)stages);
     uint64_t* const bar = (uint64_t*)(smem + L::NBUF * L::BUF + L::STAGES + L::BETA + L::STG);
+    float* const hsrc = (float*)(smem + L::NBUF * L::BUF + L::STAGES + L::BETA + L::STG + 16);
+    uint32_t* const hbeta = (uint32_t*)((unsigned char*)hsrc + L::HSRC);
     const in_t* llr = (const in_t*)llr_;
     st_t* const gst = (st_t*)gslot;
     const unsigned tid = FPC > 1 ? (threadIdx.x & 31u) : threadIdx.x;  // thread index in its group
@@ -108,6 +124,17 @@ __global__ void __launch_bounds__(T * FPC, MINB)
     if (threadIdx.x == 0 && blockIdx.x == 0) g_ptrace = T > 32 ? (unsigned long long*)gscratch : nullptr;
     __syncthreads();
 #endif
+    if constexpr (L::HELP) {
+        for (int i = threadIdx.x; i < C::WST; i += blockDim.x) hsrc[i] = 0.0f;
+        __syncthreads();
+        if (threadIdx.x >= T) {  // the helper warp: run-ahead only, never touches real data
+            for (long long g = blockIdx.x; g < n_frames; g += gridDim.x) {
+                const OpSync<T> hs{0, nullptr, 0};
+                C::template helper<P>(hsrc, hbeta, hs);
+            }
+            return;
+        }
+    }
     // frames of round r: (r * gridDim.x + blockIdx.x) * FPC + grp
     const long long stride = (long long)gridDim.x * FPC;
     long long f = (long long)blockIdx.x * FPC + grp;
@@ -119,7 +146,7 @@ __global__ void __launch_bounds__(T * FPC, MINB)
             if (f < n_frames) tma_load_1d(buf0, llr + f * N, L::FRAME_BYTES, bar);
         }
         __syncwarp();
-        if constexpr (T > 32) __syncthreads();
+        if constexpr (T > 32) group_sync<T>();
     }
     for (int it = 0; f < n_frames; f += stride, ++it) {
         // warps of this round that have a frame: they alone take part in the op barriers

@@ -127,8 +127,8 @@ static polar_status init_device(polar_code* h) {
     for (int i = 0; i < (e ? 4 : 0); ++i) {
         const void* k = *vs[i]->kern;
         CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*vs[i]->smem));
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ[i], k, (int)(vs[i]->threads * vs[i]->frames),
-                                                               *vs[i]->smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &h->occ[i], k, (int)(vs[i]->threads * vs[i]->frames + vs[i]->extra), *vs[i]->smem));
         if (h->occ[i] < 1) return fail(POLAR_ERR_CUDA, "decoder kernel variant %d cannot be resident", i);
         if (vs[i]->gscratch) {  // one slot per resident frame group of the persistent grid
             const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * vs[i]->gscratch;
@@ -326,7 +326,7 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     if (lat) gs = h->d_trace;
 #endif
     void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs};
-    CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(v.threads * v.frames), args, smem, s));
+    CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(v.threads * v.frames + v.extra), args, smem, s));
     return POLAR_OK;
 }
 

@@ -16,6 +16,7 @@ struct Variant {
     uint32_t threads;      // threads per frame group
     uint32_t frames;       // frame groups (frames decoded concurrently) per CTA
     uint32_t gscratch;     // bytes of global stage scratch per frame group (0: none)
+    uint32_t extra;        // extra threads per CTA (the latency variant's run-ahead helper warp)
 };
 
 struct RegistryEntry {
