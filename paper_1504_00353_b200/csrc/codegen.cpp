@@ -49,7 +49,8 @@ struct Spec {
     int cps = 1;          // throughput variant: CTAs per SM requested from ptxas (__launch_bounds__ min blocks)
     int wlat = 0;         // latency variant's warp-subtree size (WLAT=; default W)
     int xw = 0;           // latency variant: CTA-level nodes up to XW run on warp 0 alone (XW=)
-    bool helper = false;  // latency variant: instruction run-ahead helper warp (HELPER=1)
+    int helper = 0;       // latency variant: run-ahead helper warp on scheduler HELPER-1 (HELPER=1|2)
+    bool latni = false;   // latency variant: non-inlined subtree copies (LATNI=1)
     bool gbeta = false;   // throughput variant: decision bits in the global slot scratch too (GBETA=1)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
 };
@@ -361,15 +362,16 @@ struct CtaEmitter {
     // latency), profiles/r1_history.md.
     SharedFns* sh_lat = nullptr;
     bool helper = false;                  // HELPER: instruction run-ahead warp (latency variant)
+    bool latni = false;                   // latency-copy subtrees non-inlined
     std::vector<std::string> lat_subs;    // latency-copy subtree functions, in call order
     void sub_call(int id, const std::string& src) {
         std::string fname = "sub" + std::to_string(n_subs++);
-        if ((sh && !sh->sizes.empty() && sh_lat) || helper) {
+        if ((sh && !sh->sizes.empty() && sh_lat) || helper || latni) {
             TraceMarks* keep = g_marks;
             g_marks = nullptr;  // trace marks only in the latency copy
             emit_warp_sub(subs, t, id, fname + "_tp", sh);
             g_marks = keep;
-            emit_warp_sub(subs, t, id, fname + "_lat", sh_lat ? sh_lat : sh, false, helper);
+            emit_warp_sub(subs, t, id, fname + "_lat", sh_lat ? sh_lat : sh, false, helper || latni);
             lat_subs.push_back(fname + "_lat");
             emit("if constexpr (T == 32) { " + fname + "_tp<P>(" + src + ", beta); } else { if (gtid<T>() < 32) " +
                  fname + "_lat<P>(" + src + ", beta); }");
@@ -488,7 +490,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     if (!cta_phase) {
         o << "    static constexpr int STAGE_ELEMS = 0;\n    static constexpr int STAGE_ELEMS_SMEM = 0;\n"
           << "    static constexpr int GSTAGE_ELEMS = 0;\n    static constexpr int WST = 0;\n"
-          << "    static constexpr bool GBETA = false;\n    static constexpr bool HELPER = false;\n"
+          << "    static constexpr bool GBETA = false;\n    static constexpr int HELPER = 0;\n"
           << "    template <class P, class SyncT>\n"
           << "    static PD_INLINE void helper(const float*, uint32_t*, const SyncT&) {}\n";
         emit_warp_sub(o, t, 0, "decode_root", &sh, true);  // reads the channel
@@ -502,7 +504,8 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         SharedFns sh_none{sp.mask, {}, {}, {}};
         ce.sh_lat = &sh_none;
         ce.XW = sp.xw;
-        ce.helper = sp.helper;
+        ce.helper = sp.helper > 0;
+        ce.latni = sp.latni;
         int acc = 0, sacc = 0, gacc = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         for (int m = sp.N / 2; m >= W; m /= 2) {
@@ -522,7 +525,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
           << "    static constexpr int GSTAGE_ELEMS = " << gacc << ";\n"
           << "    static constexpr int WST = " << W << ";  // f32 stage feeding the register subtrees\n"
           << "    static constexpr bool GBETA = " << (sp.gbeta && gacc > 0 ? "true" : "false") << ";\n"
-          << "    static constexpr bool HELPER = " << (ce.helper ? "true" : "false") << ";\n";
+          << "    static constexpr int HELPER = " << (ce.helper ? sp.helper : 0) << ";  // helper warp on scheduler HELPER-1\n";
         o << subs.str();
         // the helper warp's run-ahead sequence: the latency copies of the subtrees, in call order
         o << "    template <class P, class SyncT>\n"
@@ -633,7 +636,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                     << (v.gtop ? a16(g_elems * (std::string(v.prof) == "PF32" ? 4 : 1)) +
                                      (sp.gbeta ? a16(std::max(1, sp.N / 32) * 4) : 0)
                                : 0)
-                    << ", " << (v.lat && sp.helper && sp.N > WL ? 32 : 0) << "}";
+                    << ", " << (v.lat && sp.helper && sp.N > WL ? 32 * sp.helper : 0) << "}";
     reg_entries << ", \"" << sched << "\"},\n";
 }
 
@@ -694,7 +697,8 @@ int main(int argc, char** argv) {
             else if (opt.rfind("CPS=", 0) == 0) sp.cps = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("WLAT=", 0) == 0) sp.wlat = std::atoi(opt.c_str() + 5);
             else if (opt.rfind("XW=", 0) == 0) sp.xw = std::atoi(opt.c_str() + 3);
-            else if (opt.rfind("HELPER=", 0) == 0) sp.helper = std::atoi(opt.c_str() + 7) != 0;
+            else if (opt.rfind("HELPER=", 0) == 0) sp.helper = std::atoi(opt.c_str() + 7);
+            else if (opt.rfind("LATNI=", 0) == 0) sp.latni = std::atoi(opt.c_str() + 6) != 0;
             else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();

@@ -71,7 +71,7 @@ struct FrameLayout {
     static constexpr int WST_OFF = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t));
     static constexpr int STAGES = WST_OFF + (WF32 ? align16(C::WST * (int)sizeof(typename P::v_t)) : 0);
     // helper warp (latency variant, Code::HELPER): dummy subtree input and decision bits
-    static constexpr bool HELP = WF32 && C::HELPER;
+    static constexpr bool HELP = WF32 && C::HELPER > 0;
     static constexpr int HSRC = HELP ? align16(C::WST * 4) : 0;
     static constexpr int HBETA = HELP ? align16((C::N >= 32 ? C::N / 32 : 1) * 4) : 0;
     // GTOP && C::GBETA: the decision bits also live in the frame slot's global scratch
@@ -91,7 +91,7 @@ struct FrameLayout {
 // GTOP: the largest stages (N/2 and N/4 by default) live in global scratch (L2-resident), one slot per frame
 // group of the persistent grid, so that more frames fit in shared memory per SM.
 template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP, int MINB = 1>
-__global__ void __launch_bounds__(T * FPC + (T > 32 && C::HELPER ? 32 : 0), MINB)
+__global__ void __launch_bounds__(T * FPC + (T > 32 ? 32 * C::HELPER : 0), MINB)
     k_frame(const void* __restrict__ llr_, long long n_frames, uint32_t* __restrict__ out,
             const uint32_t* __restrict__ gtab, void* __restrict__ gscratch) {
     static_assert(FPC == 1 || T == 32, "");
@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(T * FPC + (T > 32 && C::HELPER ? 32 : 0), MINB
         for (int i = threadIdx.x; i < C::WST; i += blockDim.x) hsrc[i] = 0.0f;
         __syncthreads();
         if (threadIdx.x >= T) {  // the helper warp: run-ahead only, never touches real data
+            if (threadIdx.x < T + 32 * (C::HELPER - 1)) return;  // spacer warps put it on scheduler HELPER-1
             for (long long g = blockIdx.x; g < n_frames; g += gridDim.x) {
                 const OpSync<T> hs{0, nullptr, 0};
                 C::template helper<P>(hsrc, hbeta, hs);
