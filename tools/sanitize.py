@@ -1,0 +1,38 @@
+"""Small decodes for compute-sanitizer runs (memcheck / racecheck / synccheck / initcheck):
+each registered code family and kernel variant (throughput, latency, generic) on a few
+frames, checked against the oracle.   usage: compute-sanitizer --tool X python tools/sanitize.py"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_1504_00353_b200 as pb  # noqa: E402
+from seeded_inputs import random_llr_i8, random_mask  # noqa: E402
+
+CASES = [(8, 5, None), (1024, 512, 2.5), (2048, 1723, 4.0), (4096, 2048, 2.5), (8192, 6000, 3.5), (32768, 29492, 4.5)]
+bad = 0
+for N, K, e in CASES:
+    mask = np.array([1, 1, 0, 0, 1, 0, 0, 0], np.uint8) if e is None else oracle.construct_ga(N, K, e)
+    code = pb.PolarCode(N, K, mask)
+    n = 7 if N >= 8192 else 37
+    x = random_llr_i8(N + 1, (n, N), -60, 60)
+    want = oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, x)))
+    for variant in ("throughput", "latency", "generic"):
+        code.set_variant(variant)
+        for prof in ("i8", "f32"):
+            t = torch.from_numpy(x if prof == "i8" else x.astype(np.float32)).cuda()
+            out = (code.decode_i8(t) if prof == "i8" else code.decode_f32(t)).cpu().numpy().view(np.uint32)
+            ok = np.array_equal(out, want)
+            bad += not ok
+            print(f"({N},{K}) {variant:10s} {prof}: {'ok' if ok else 'MISMATCH'}", flush=True)
+m = random_mask(5, 256, 100)
+code = pb.PolarCode(256, 100, m)
+x = random_llr_i8(9, (5, 256))
+ok = np.array_equal(code.decode_i8(torch.from_numpy(x).cuda()).cpu().numpy().view(np.uint32),
+                    oracle.pack_bits(oracle.info_bits(m, oracle.fastssc_decode(m, x))))
+bad += not ok
+print("generic random mask:", "ok" if ok else "MISMATCH")
+sys.exit(1 if bad else 0)
