@@ -19,13 +19,14 @@ for N, K, e in CASES:
     code = pb.PolarCode(N, K, mask)
     n = 7 if N >= 8192 else 37
     x = random_llr_i8(N + 1, (n, N), -60, 60)
-    want = oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, x)))
+    xs = {"i8": x, "f32": x.astype(np.float32)}
+    want = {p: oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, v))) for p, v in xs.items()}
     for variant in ("throughput", "latency", "generic"):
         code.set_variant(variant)
         for prof in ("i8", "f32"):
-            t = torch.from_numpy(x if prof == "i8" else x.astype(np.float32)).cuda()
+            t = torch.from_numpy(xs[prof]).cuda()
             out = (code.decode_i8(t) if prof == "i8" else code.decode_f32(t)).cpu().numpy().view(np.uint32)
-            ok = np.array_equal(out, want)
+            ok = np.array_equal(out, want[prof])
             bad += not ok
             print(f"({N},{K}) {variant:10s} {prof}: {'ok' if ok else 'MISMATCH'}", flush=True)
 m = random_mask(5, 256, 100)
