@@ -293,11 +293,13 @@ struct Chunk<PI8, CE> {
     // G: h = sat(b + (beta ? -h : h)); bit k of `bits` is beta of element k; the saturation
     // is min.xorsign.abs against 127.
     PD_INLINE void g(const Chunk& b, uint32_t bits) {
+        // sign mask of the pair (2q, 2q+1): t = its 2 bits; t * 0x40008000 = (t << 15) + (t << 30)
+        // (no overlapping terms, so no carries) puts bit 0 at 15 and bit 1 at 31; the mask keeps
+        // those two (one IMAD on the FMA pipe instead of two shifts and three logic ops).
 #pragma unroll
         for (int q = 0; q < CE / 2; ++q) {
-            const uint32_t lo = (bits << (15 - 2 * q)) & 0x8000u;
-            const uint32_t hi = (bits << (30 - 2 * q)) & 0x80000000u;
-            h[q] = h2minxs(h2add(b.h[q], h[q] ^ (lo | hi)), 0x57F057F0u);
+            const uint32_t m = (((bits >> (2 * q)) & 3u) * 0x40008000u) & 0x80008000u;
+            h[q] = h2minxs(h2add(b.h[q], h[q] ^ m), 0x57F057F0u);
         }
     }
     PD_INLINE void g0(const Chunk& b) {
