@@ -203,17 +203,19 @@ def main():
     def max_over_ranks(x: float) -> float:
         return _mor(x, dev)
 
-    def throughput(code_t, B, steps, warmup, with_e2e):
+    def throughput(code_t, B, steps, warmup, with_e2e, prof="i8"):
         N, K, e = code_t
         code = pb.PolarCode.ga(N, K, e)
-        llr = torch.empty(B, N, dtype=torch.int8, device=dev)
+        llr = torch.empty(B, N, dtype=torch.int8 if prof == "i8" else torch.float32, device=dev)
         truth = torch.empty(B, code.info_words, dtype=torch.int32, device=dev)
         out = torch.empty(B, code.info_words, dtype=torch.int32, device=dev)
         first, _ = frame_range(rank, ws, B)  # weak scaling: disjoint global frame ranges
-        code.gen_bpsk_awgn(SEED, first, B, e, 4.0, llr_i8=llr, info=truth)
+        code.gen_bpsk_awgn(SEED, first, B, e, 4.0, llr_i8=llr if prof == "i8" else None,
+                           llr_f32=llr if prof == "f32" else None, info=truth)
+        decode = code.decode_i8 if prof == "i8" else code.decode_f32
         stream = torch.cuda.current_stream()
         for _ in range(warmup):
-            code.decode_i8(llr, out)
+            decode(llr, out)
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
@@ -224,7 +226,7 @@ def main():
             t0.record(stream)
             for i in range(steps):
                 ev[i][0].record(stream)
-                code.decode_i8(llr, out)
+                decode(llr, out)
                 ev[i][1].record(stream)
             t1.record(stream)
             torch.cuda.synchronize()
@@ -289,6 +291,11 @@ def main():
         r2 = throughput(CODE2, BATCH2, max(3, args.steps // 2), args.warmup, with_e2e=False)
         extra["c2048_1723_i8"] = {"info_gbps": r2["gbps"], "frames_per_s": ws * r2["B"] / (r2["ms_per_step"] * 1e-3),
                                   "batch_per_gpu": r2["B"], "ms_per_step": r2["ms_per_step"], "fer": r2["fer"]}
+        # f32 profile throughput of both codes (same frames as LLR floats)
+        for tag, code_t, B in (("c32768_29492_f32", CODE, args.batch // 2), ("c2048_1723_f32", CODE2, BATCH2 // 4)):
+            r3 = throughput(code_t, B, max(3, args.steps // 2), args.warmup, with_e2e=False, prof="f32")
+            extra[tag] = {"info_gbps": r3["gbps"], "frames_per_s": ws * r3["B"] / (r3["ms_per_step"] * 1e-3),
+                          "batch_per_gpu": r3["B"], "ms_per_step": r3["ms_per_step"], "fer": r3["fer"]}
         extra["latency_batch1_32768_29492"] = latency_batch1(CODE)
         extra["latency_batch1_2048_1723"] = latency_batch1(CODE2)
     N, K = main_r["N"], main_r["K"]
