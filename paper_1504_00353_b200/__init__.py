@@ -160,7 +160,7 @@ class PolarCode:
 
     def set_variant(self, variant: str) -> None:
         """'auto' | 'throughput' | 'latency' | 'generic' (all decode identically)."""
-        _check(lib().polar_code_set_variant(self._h, {"auto": 0, "throughput": 1, "latency": 2, "generic": 3}[variant]))
+        _check(lib().polar_code_set_variant(self._h, {"auto": 0, "throughput": 1, "latency": 2, "generic": 3, "xframe": 4}[variant]))
 
     def mask(self) -> np.ndarray:
         m = np.zeros(self.N, np.uint8)

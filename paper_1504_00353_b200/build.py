@@ -31,7 +31,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-I", CSRC, "-I", INCLUDE,
                   "-Xptxas", "-v", "--resource-usage"] + EXTRA
-HEADERS = ["decoder.cuh", "kernels.cuh", "registry.hpp", "tree.hpp"]
+HEADERS = ["decoder.cuh", "kernels.cuh", "xframe.cuh", "registry.hpp", "tree.hpp"]
 
 
 def _run(cmd, log=None):

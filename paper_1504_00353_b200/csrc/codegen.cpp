@@ -53,6 +53,9 @@ struct Spec {
     bool latni = false;   // latency variant: non-inlined subtree copies (LATNI=1)
     bool gbeta = false;   // throughput variant: decision bits in the global slot scratch too (GBETA=1)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
+    int xsm = 48 * 1024;  // frame-interleaved variant: shared-memory budget per warp (XSM=; 24K/48K/72K
+                          // measured 162/262/207 Gbps at (2048,1723), profiles/r1_history.md)
+    int xwpc = 1;         // frame-interleaved variant: warps per CTA (XWPC=)
 };
 
 // Distinct small-subtree patterns emitted once as __noinline__ device functions, so that the
@@ -460,6 +463,181 @@ struct CtaEmitter {
     }
 };
 
+// Frame-interleaved decoder (xframe.cuh): the same Fast-SSC traversal, emitted as per-lane
+// code, one frame per lane.  Nodes of N_v >= 64 are stage ops on interleaved int8 stages
+// (shared memory, or the warp's global scratch slot for the largest ones); a node of N_v = 64
+// feeds its two 32-value children straight into f32 registers, where the subtree runs as
+// compile-time-indexed scalar code (lF/lG/lR1/lRep/lSPC of decoder.cuh).
+struct XEmitter {
+    const Tree& t;
+    std::ostringstream& o;
+    std::map<int, std::pair<std::string, int>> stage;  // child size -> (space, byte offset per warp)
+    int nm = 0;
+    std::string ind = "        ";
+
+    std::string fresh(const char* p) { return std::string(p) + std::to_string(nm++); }
+    const std::vector<uint8_t>* mask = nullptr;
+    std::map<std::string, std::string>* fns = nullptr;  // frozen pattern of a 64-node -> function
+    std::ostringstream* defs = nullptr;
+
+    // A split 64-node whose two 32-value children run in registers, as a __noinline__ function
+    // of its parent pointer and beta words (one per distinct frozen pattern: less code to fetch
+    // and to compile).
+    std::string pair_fn(int id) {
+        const Node& v = t.nodes[id];
+        std::string key;
+        for (int i = v.off; i < v.off + v.n; ++i) key += (*mask)[i] ? '1' : '0';
+        auto it = fns->find(key);
+        if (it != fns->end()) return it->second;
+        const std::string fn = "xp" + std::to_string(fns->size());
+        (*fns)[key] = fn;
+        std::ostringstream body;
+        XEmitter e{t, body};
+        e.ind = "    ";
+        const Node& l = t.nodes[v.left];
+        const Node& r = t.nodes[v.right];
+        body << "    float q[32];\n";
+        if (l.kind == Kind::Rate0) {
+            body << "    xf::rG0R<S>(p, q);\n";
+            const std::string mr = e.reg(v.right, "q");
+            body << "    bp[0] = " << mr << ";\n    bp[32] = " << mr << ";\n";
+        } else {
+            body << "    xf::rF<S>(p, q);\n";
+            const std::string ml = e.reg(v.left, "q");
+            if (r.kind == Kind::Rate0) {
+                body << "    bp[0] = " << ml << ";\n    bp[32] = 0u;\n";
+            } else {
+                body << "    xf::rG<S>(p, q, " << ml << ");\n";
+                const std::string mr = e.reg(v.right, "q");
+                body << "    bp[0] = " << ml << " ^ " << mr << ";\n    bp[32] = " << mr << ";\n";
+            }
+        }
+        *defs << "template <int S>\n__device__ __noinline__ void " << fn << "(const int8_t* p, uint32_t* bp) {\n"
+              << body.str() << "}\n\n";
+        return fn;
+    }
+
+    // Register node (n <= 32) whose values are in array `arr`; returns its beta mask name.
+    std::string reg(int id, const std::string& arr) {
+        const Node& v = t.nodes[id];
+        const int n = v.n;
+        const std::string N_ = std::to_string(n);
+        std::string m;
+        switch (v.kind) {
+            case Kind::Rate0: return "0u";
+            case Kind::Rate1: m = fresh("m"); o << ind << "const uint32_t " << m << " = lR1<PI8, " << N_ << ">(" << arr << ");\n"; return m;
+            case Kind::Rep: m = fresh("m"); o << ind << "const uint32_t " << m << " = lRep<PI8, " << N_ << ">(" << arr << ");\n"; return m;
+            case Kind::Spc: m = fresh("m"); o << ind << "const uint32_t " << m << " = lSPC<PI8, " << N_ << ">(" << arr << ");\n"; return m;
+            case Kind::Split: break;
+        }
+        const int h = n / 2;
+        const std::string H = std::to_string(h);
+        const std::string c = fresh("q");
+        o << ind << "float " << c << "[" << h << "];\n";
+        const Node& l = t.nodes[v.left];
+        const Node& r = t.nodes[v.right];
+        if (l.kind == Kind::Rate0) {
+            o << ind << "lG0R<PI8, " << N_ << ">(" << arr << ", " << c << ");\n";
+            const std::string mr = reg(v.right, c);
+            m = fresh("m");
+            o << ind << "const uint32_t " << m << " = " << mr << " | (" << mr << " << " << H << ");\n";
+            return m;
+        }
+        o << ind << "lF<PI8, " << N_ << ">(" << arr << ", " << c << ");\n";
+        const std::string ml = reg(v.left, c);
+        if (r.kind == Kind::Rate0) return ml;
+        o << ind << "lG<PI8, " << N_ << ">(" << arr << ", " << c << ", " << ml << ");\n";
+        const std::string mr = reg(v.right, c);
+        m = fresh("m");
+        o << ind << "const uint32_t " << m << " = (" << ml << " ^ " << mr << ") | (" << mr << " << " << H << ");\n";
+        return m;
+    }
+
+    // Memory node (n >= 64) whose values are the stage `S` at byte offset SO ("CH": channel).
+    void mem(int id, const std::string& S, int SO) {
+        const Node& v = t.nodes[id];
+        const int n = v.n, b = v.off;
+        const std::string N_ = std::to_string(n), B = std::to_string(b);
+        const std::string src = S + ", " + std::to_string(SO);
+        switch (v.kind) {
+            case Kind::Rate0: return;
+            case Kind::Rate1: o << ind << "xf::lvR1<" << N_ << ", " << src << ">(x, " << B << ");\n"; return;
+            case Kind::Rep: o << ind << "xf::lvRep<" << N_ << ", " << src << ">(x, " << B << ");\n"; return;
+            case Kind::Spc: o << ind << "xf::lvSPC<" << N_ << ", " << src << ">(x, " << B << ");\n"; return;
+            case Kind::Split: break;
+        }
+        const int h = n / 2;
+        const Node& l = t.nodes[v.left];
+        const Node& r = t.nodes[v.right];
+        if (h == 32) {  // both children in registers: one shared function per frozen pattern
+            const std::string fn = pair_fn(id);
+            o << ind << "xfn::" << fn << "<" << S << ">(xf::cptr<" << src << ">(x, 0), xf::bword(x, " << b / 32 << "));\n";
+            return;
+        }
+        const auto& d = stage.at(h);
+        const std::string dst = d.first + ", " + std::to_string(d.second);
+        const std::string targs = N_ + ", " + src + ", " + dst;
+        if (l.kind == Kind::Rate0) {
+            o << ind << "xf::sG0R<" << targs << ">(x);\n";
+            mem(v.right, d.first, d.second);
+            o << ind << "xf::bComb0R<" << N_ << ">(x, " << B << ");\n";
+            return;
+        }
+        o << ind << "xf::sF<" << targs << ">(x);\n";
+        mem(v.left, d.first, d.second);
+        if (r.kind == Kind::Rate0) {
+            o << ind << "xf::bZero<" << h / 32 << ">(x, " << (b + h) / 32 << ");\n";
+            return;
+        }
+        o << ind << "xf::sG<" << targs << ">(x, " << B << ");\n";
+        mem(v.right, d.first, d.second);
+        o << ind << "xf::bComb<" << N_ << ">(x, " << B << ");\n";
+    }
+};
+
+// Emit struct XCode (frame-interleaved int8 decoder).  Stages of size >= xg live in the
+// warp's global scratch slot (L2), smaller ones in shared memory; beta in shared memory when
+// its 4N bytes per warp fit under the budget, else in the global slot.
+void emit_xcode(std::ostringstream& o, const Tree& t, const Spec& sp, int xg, bool beta_gl) {
+    XEmitter e{t, o};
+    int sacc = 0, gacc = 0;
+    for (int m = sp.N / 2; m >= 64; m /= 2) {
+        if (m >= xg) {
+            e.stage[m] = {"xf::GL", gacc};
+            gacc += 32 * m;
+        } else {
+            e.stage[m] = {"xf::SM", sacc};
+            sacc += 32 * m;
+        }
+    }
+    const int beta = 4 * 32 * std::max(1, sp.N / 32);
+    std::ostringstream body, defs;
+    std::map<std::string, std::string> fns;
+    XEmitter eb{t, body};
+    eb.stage = e.stage;
+    eb.mask = &sp.mask;
+    eb.fns = &fns;
+    eb.defs = &defs;
+    if (sp.N <= 32) {
+        body << "        float q[" << sp.N << "];\n        xf::rChan<" << sp.N << ">(x, q);\n";
+        const std::string m = eb.reg(0, "q");
+        body << "        xf::stB(x, 0, " << m << ");\n";
+    } else {
+        eb.mem(0, "xf::CH", 0);
+    }
+    o << "namespace xfn {\nusing namespace pd;\n" << defs.str() << "}  // namespace xfn\n\n";
+    o << "struct XCode {\n"
+      << "    static constexpr int N = " << sp.N << ";\n"
+      << "    static constexpr int K = " << sp.K << ";\n"
+      << "    static constexpr int SSTAGE = " << sacc << ";  // shared stage bytes per warp\n"
+      << "    static constexpr int GSTAGE = " << gacc << ";  // global stage bytes per warp slot\n"
+      << "    static constexpr bool BETA_GL = " << (beta_gl ? "true" : "false") << ";\n"
+      << "    static constexpr int SMEM_WARP = SSTAGE + (BETA_GL ? 0 : " << beta << ");\n"
+      << "    static constexpr int GSLOT = GSTAGE + (BETA_GL ? " << beta << " : 0);\n"
+      << "    static PD_INLINE void decode(const xf::Ctx& x) {\n"
+      << body.str() << "    }\n};\n\n";
+}
+
 std::string mask_string(const std::vector<uint8_t>& m) {
     std::string s;
     for (uint8_t b : m) s += b ? '1' : '0';
@@ -552,13 +730,26 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     } else {
         emit_struct("Code", W);
     }
+    // frame-interleaved variant: the largest stages go to the global slot until the shared
+    // stages (and beta, unless it is global too) fit the per-warp budget
+    int xg = sp.N;  // stages of size >= xg are global
+    const int xbeta = 4 * 32 * std::max(1, sp.N / 32);
+    const bool xbeta_gl = xbeta > sp.xsm / 2;
+    auto xsmem = [&](int g) {
+        int s = xbeta_gl ? 0 : xbeta;
+        for (int m = sp.N / 2; m >= 64; m /= 2)
+            if (m < g) s += 32 * m;
+        return s;
+    };
+    while (xg > 64 && xsmem(xg) > sp.xsm) xg /= 2;
+    emit_xcode(o, t, sp, xg, xbeta_gl);
     o << "}  // namespace code_" << sp.name << "\n}  // namespace pd\n\n";
     {
         std::ostringstream head;
         head << "// Generated by codegen.cpp for code " << sp.name << " (N=" << sp.N << ", K=" << sp.K << ", "
              << ops.size() << " Fast-SSC ops, W=" << W << ", " << sh.by_key.size()
              << " shared subtree functions). Do not edit.\n"
-             << "#include \"kernels.cuh\"\n\nnamespace pd {\nnamespace code_" << sp.name << " {\n\n"
+             << "#include \"kernels.cuh\"\n#include \"xframe.cuh\"\n\nnamespace pd {\nnamespace code_" << sp.name << " {\n\n"
              << sh.defs.str();
         const std::string rest = o.str();
         o.str("");
@@ -616,6 +807,16 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         reg_decl << "extern const void* const polar_kern_" << sp.name << "_" << v.tag << ";\n"
                  << "extern const unsigned polar_smem_" << sp.name << "_" << v.tag << ";\n";
     }
+    {
+        const std::string XC = "pd::code_" + sp.name + "::XCode";
+        const std::string kx = "pd::k_xf<" + XC + ", " + std::to_string(sp.xwpc) + ", 1>";
+        o << "extern const void* const polar_kern_" << sp.name << "_xf_i8 = (const void*)&" << kx << ";\n"
+          << "extern const unsigned polar_smem_" << sp.name << "_xf_i8 = " << sp.xwpc << " * " << XC << "::SMEM_WARP;\n"
+          << "extern const unsigned polar_gslot_" << sp.name << "_xf_i8 = " << XC << "::GSLOT;\n";
+        reg_decl << "extern const void* const polar_kern_" << sp.name << "_xf_i8;\n"
+                 << "extern const unsigned polar_smem_" << sp.name << "_xf_i8;\n"
+                 << "extern const unsigned polar_gslot_" << sp.name << "_xf_i8;\n";
+    }
     std::ofstream(outdir + "/code_" + sp.name + ".cu") << o.str();
     {
         std::ofstream tl(outdir + "/trace_" + sp.name + ".txt");
@@ -637,6 +838,8 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                                      (sp.gbeta ? a16(std::max(1, sp.N / 32) * 4) : 0)
                                : 0)
                     << ", " << (v.lat && sp.helper && sp.N > WL ? 32 * sp.helper : 0) << "}";
+    reg_entries << ", {&polar_kern_" << sp.name << "_xf_i8, &polar_smem_" << sp.name << "_xf_i8, 32, " << sp.xwpc
+                << ", 0, 0}, &polar_gslot_" << sp.name << "_xf_i8";
     reg_entries << ", \"" << sched << "\"},\n";
 }
 
@@ -699,6 +902,8 @@ int main(int argc, char** argv) {
             else if (opt.rfind("XW=", 0) == 0) sp.xw = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("HELPER=", 0) == 0) sp.helper = std::atoi(opt.c_str() + 7);
             else if (opt.rfind("LATNI=", 0) == 0) sp.latni = std::atoi(opt.c_str() + 6) != 0;
+            else if (opt.rfind("XSM=", 0) == 0) sp.xsm = std::atoi(opt.c_str() + 4);
+            else if (opt.rfind("XWPC=", 0) == 0) sp.xwpc = std::atoi(opt.c_str() + 5);
             else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();

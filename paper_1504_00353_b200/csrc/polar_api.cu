@@ -66,11 +66,11 @@ struct polar_code {
     bool dev_ready = false;
     int device = -1;
     int n_sm = 0;
-    int occ[4] = {0, 0, 0, 0};    // resident CTAs per SM: tp_f32, tp_i8, lat_f32, lat_i8
-    int variant = 0;              // 0 auto, 1 throughput, 2 latency (polar_code_set_variant)
+    int occ[5] = {0, 0, 0, 0, 0};  // resident CTAs per SM: tp_f32, tp_i8, lat_f32, lat_i8, xf_i8
+    int variant = 0;              // 0 auto, 1 throughput, 2 latency, 3 generic, 4 frame-interleaved
     uint16_t* d_pos = nullptr;    // K information positions, ascending (encoder / generator)
     uint32_t* d_gtab = nullptr;   // gather table: info mask words, then info-bit prefix per word
-    void* d_gscratch[4] = {nullptr, nullptr, nullptr, nullptr};  // per variant global stage scratch
+    void* d_gscratch[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // per variant global stage scratch
     unsigned long long* d_trace = nullptr;  // POLAR_TRACE builds: per-op clock64 of the latency variant
     uint32_t* d_info_mask = nullptr;  // N/32 words (>= 1), bit set = information position
     // host-buffer path (lazily allocated, guarded by mu)
@@ -117,21 +117,23 @@ static polar_status init_device(polar_code* h) {
         CUDA_TRY(cudaMalloc(&h->d_prog, std::max<size_t>(1, h->prog.size()) * sizeof(uint32_t)));
         CUDA_TRY(cudaMemcpy(h->d_prog, h->prog.data(), h->prog.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     }
-    const Variant* vs[4] = {nullptr, nullptr, nullptr, nullptr};
+    const Variant* vs[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     if (e) {
         vs[0] = &e->tp_f32;
         vs[1] = &e->tp_i8;
         vs[2] = &e->lat_f32;
         vs[3] = &e->lat_i8;
+        vs[4] = &e->xf_i8;
     }
-    for (int i = 0; i < (e ? 4 : 0); ++i) {
+    for (int i = 0; i < (e ? 5 : 0); ++i) {
         const void* k = *vs[i]->kern;
         CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*vs[i]->smem));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &h->occ[i], k, (int)(vs[i]->threads * vs[i]->frames + vs[i]->extra), *vs[i]->smem));
         if (h->occ[i] < 1) return fail(POLAR_ERR_CUDA, "decoder kernel variant %d cannot be resident", i);
-        if (vs[i]->gscratch) {  // one slot per resident frame group of the persistent grid
-            const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * vs[i]->gscratch;
+        const size_t slot = i == 4 ? *e->xf_gslot : vs[i]->gscratch;
+        if (slot) {  // one slot per resident frame group (xf: per warp) of the persistent grid
+            const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * slot;
             CUDA_TRY(cudaMalloc(&h->d_gscratch[i], bytes));
         }
     }
@@ -208,7 +210,7 @@ extern "C" void polar_code_destroy(polar_code* h) {
         cudaFree(h->d_pos);
         cudaFree(h->d_info_mask);
         cudaFree(h->d_gtab);
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 5; ++i)
             if (h->d_gscratch[i]) cudaFree(h->d_gscratch[i]);
         for (int i = 0; i < 2; ++i) {
             if (h->d_stage_llr[i]) cudaFree(h->d_stage_llr[i]);
@@ -237,7 +239,7 @@ extern "C" polar_status polar_code_is_specialised(const polar_code* h, int* spec
 }
 
 extern "C" polar_status polar_code_set_variant(polar_code* h, int variant) {
-    if (!h || variant < 0 || variant > 3) return fail(POLAR_ERR_INVALID_ARGUMENT, "variant must be 0, 1, 2 or 3");
+    if (!h || variant < 0 || variant > 4) return fail(POLAR_ERR_INVALID_ARGUMENT, "variant must be 0, 1, 2, 3 or 4");
     h->variant = variant;
     return POLAR_OK;
 }
@@ -312,6 +314,22 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     // (measured crossover, profiles/r1_sweeps.md: at N >= 16384 one latency wave of #SMs
     // frames takes ~1/4 of a throughput wave)
     const int64_t lat_max = (int64_t)h->n_sm * (h->N >= 16384 ? 4 : 1);
+    // Frame-interleaved variant (a lane per frame): forced by variant 4; automatic for int8
+    // codes with N <= 1024 once the batch fills every SM with several 32-frame warps
+    // (measured faster there only: (1024,512) 172 vs 146 Gbps; (2048,1723) 262 vs 316).
+    const bool xf = i8 && (h->variant == 4 || (h->variant == 0 && h->N <= 1024 && n >= (int64_t)h->n_sm * 32 * 4));
+    if (xf) {  // 32 frames per warp, frames = warps per CTA
+        const Variant& v = e->xf_i8;
+        const int64_t groups = (n + 31) / 32;
+        const int64_t resident = (int64_t)h->occ[4] * h->n_sm;
+        const unsigned grid = (unsigned)std::min<int64_t>((groups + v.frames - 1) / v.frames, resident);
+        long long nn = (long long)n;
+        const uint32_t* gtab = h->d_gtab;
+        void* gs = h->d_gscratch[4];
+        void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs};
+        CUDA_TRY(cudaLaunchKernel(*v.kern, dim3(grid), dim3(32 * v.frames), args, *v.smem, s));
+        return POLAR_OK;
+    }
     const bool lat = h->variant == 2 || (h->variant == 0 && n <= lat_max);
     const int vi = (lat ? 2 : 0) + (i8 ? 1 : 0);
     const Variant& v = vi == 0 ? e->tp_f32 : vi == 1 ? e->tp_i8 : vi == 2 ? e->lat_f32 : e->lat_i8;

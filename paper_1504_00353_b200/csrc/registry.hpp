@@ -28,6 +28,8 @@ struct RegistryEntry {
     uint32_t warp_root;    // W: size of the subtrees decoded by one warp in registers
     Variant tp_f32, tp_i8;    // throughput: one warp per frame
     Variant lat_f32, lat_i8;  // latency: one CTA of threads per frame
+    Variant xf_i8;            // frame-interleaved throughput: one lane per frame (frames = warps per CTA)
+    const unsigned* xf_gslot; // its global scratch bytes per warp
     const char* schedule;     // ';'-separated Listing-1 op list
 };
 

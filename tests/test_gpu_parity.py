@@ -71,8 +71,10 @@ def assert_same(got, want, what):
 
 @pytest.mark.parametrize("name,N,K,mask,ebn0", CODES, ids=[c[0] for c in CODES])
 @pytest.mark.parametrize("prof", ["f32", "i8"])
-@pytest.mark.parametrize("variant", ["throughput", "latency"])
+@pytest.mark.parametrize("variant", ["throughput", "latency", "xframe"])
 def test_parity_awgn_frames(name, N, K, mask, ebn0, prof, variant):
+    if variant == "xframe" and prof == "f32":
+        pytest.skip("the frame-interleaved variant is int8 only (f32 runs the throughput kernel)")
     code = pb.PolarCode(N, K, mask)
     code.set_variant(variant)
     n = _n_frames(N)
@@ -83,7 +85,7 @@ def test_parity_awgn_frames(name, N, K, mask, ebn0, prof, variant):
 
 
 @pytest.mark.parametrize("name,N,K,mask,ebn0", CODES, ids=[c[0] for c in CODES])
-@pytest.mark.parametrize("variant", ["throughput", "latency"])
+@pytest.mark.parametrize("variant", ["throughput", "latency", "xframe"])
 def test_parity_adversarial_llrs(name, N, K, mask, ebn0, variant):
     code = pb.PolarCode(N, K, mask)
     code.set_variant(variant)
@@ -142,14 +144,17 @@ def test_generic_variant_equals_oracle_on_registered_codes(name, N, K, mask, ebn
         assert_same(gpu_decode(code, x), expected(mask, x), f"{name} generic {x.dtype}")
 
 
-def test_ragged_batches_and_grid_striding():
-    """Frame counts that are not multiples of the CTA's frames and exceed one resident wave."""
+@pytest.mark.parametrize("variant", ["auto", "xframe"])
+def test_ragged_batches_and_grid_striding(variant):
+    """Frame counts that are not multiples of the CTA's (or warp's 32) frames and exceed one
+    resident wave."""
     for (N, K, e) in [(64, 32, 2.0), (1024, 512, 2.5), (4096, 2048, 2.5)]:
         mask = oracle.construct_ga(N, K, e)
         code = pb.PolarCode(N, K, mask)
-        n = {64: 40013, 1024: 6007, 4096: 1201}[N]
+        code.set_variant(variant)
+        n = {64: 40013, 1024: 6007 if variant == "auto" else 20011, 4096: 1201}[N]
         x = random_llr_i8(21, (n, N), -40, 40)
-        assert_same(gpu_decode(code, x), expected(mask, x), f"({N},{K}) x{n}")
+        assert_same(gpu_decode(code, x), expected(mask, x), f"({N},{K}) x{n} {variant}")
 
 
 def test_zero_frames_is_noop_and_bad_pointers_rejected():

@@ -4,7 +4,7 @@
 NAME=$1; SKIP=$2; shift 3
 OUT=gpurun_out
 mkdir -p $OUT
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_frame -s $SKIP -c 1 -f -o $OUT/$NAME "$@" > $OUT/$NAME.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_frame} -s $SKIP -c 1 -f -o $OUT/$NAME "$@" > $OUT/$NAME.log 2>&1
 echo "ncu $NAME rc=$?"
 ncu -i $OUT/$NAME.ncu-rep --page details --csv > $OUT/${NAME}_details.csv 2>/dev/null
 ncu -i $OUT/$NAME.ncu-rep --page raw --csv > $OUT/${NAME}_raw.csv 2>/dev/null

@@ -15,8 +15,10 @@ ap.add_argument("--ebn0", type=float, default=4.5)
 ap.add_argument("--batch", type=int, default=4096)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--prof", default="i8", choices=["i8", "f32"])
+ap.add_argument("--variant", default="auto", choices=["auto", "throughput", "latency", "generic", "xframe"])
 a = ap.parse_args()
 code = pb.PolarCode.ga(a.N, a.K, a.ebn0)
+code.set_variant(a.variant)
 dt = torch.int8 if a.prof == "i8" else torch.float32
 llr = torch.empty(a.batch, a.N, dtype=dt, device="cuda")
 code.gen_bpsk_awgn(1504000353, 0, a.batch, a.ebn0, 4.0, **({"llr_i8": llr} if a.prof == "i8" else {"llr_f32": llr}))
