@@ -85,6 +85,60 @@ def fer(a):
                               "oracle_checked_frames": checked, "seconds": round(time.time() - t0, 2)}), flush=True)
 
 
+def ferfast(a):
+    """FER segment for the FER-1e-8 regime: frames [first, first + max)
+    at one Eb/N0, errors counted on the device (polar_count_errors); only error frames (and a few
+    random ones) come back to the host, where the oracle re-decodes them bit for bit.  Segments
+    over disjoint frame ranges are independent samples and add up."""
+    N, K = map(int, a.code.split(","))
+    code = pb.PolarCode.ga(N, K, a.design)
+    mask = code.mask()
+    W = code.info_words
+    chunk = a.chunk
+    e = float(a.points)
+    prof = "f32" if a.f32 else "i8"
+    x = torch.empty(chunk, N, dtype=torch.float32 if a.f32 else torch.int8, device="cuda")
+    truth = torch.empty(chunk, W, dtype=torch.int32, device="cuda")
+    out = torch.empty(chunk, W, dtype=torch.int32, device="cuda")
+    ctr = torch.zeros(3, dtype=torch.int64, device="cuda")
+    rng = np.random.default_rng(a.first_frame + 11)
+    frames = checked = 0
+    err_frames = []
+    t0 = time.time()
+    dec = code.decode_f32 if a.f32 else code.decode_i8
+    while frames < a.max_frames and time.time() - t0 < a.max_seconds:
+        n = min(chunk, a.max_frames - frames)
+        first = a.first_frame + frames
+        code.gen_bpsk_awgn(SEED, first, n, e, 4.0, llr_f32=x[:n] if a.f32 else None,
+                           llr_i8=None if a.f32 else x[:n], info=truth[:n])
+        dec(x[:n], out[:n])
+        before = int(ctr[2])
+        code.count_errors(out[:n], truth[:n], ctr)
+        nerr = int(ctr[2]) - before
+        idx = []
+        if nerr:
+            bad = (out[:n] != truth[:n]).any(dim=1).nonzero().flatten().cpu().numpy()
+            err_frames += [int(first + i) for i in bad]
+            idx = list(bad[: a.check])
+        if (frames // chunk) % 64 == 0:
+            idx += list(rng.choice(n, 2, replace=False))
+        if idx:
+            idx = np.unique(np.array(idx, dtype=np.int64))
+            sample = x[torch.from_numpy(idx).cuda()].cpu().numpy()
+            want = oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, sample, threads=os.cpu_count())))
+            got = out[:n][torch.from_numpy(idx).cuda()].cpu().numpy().view(np.uint32)
+            if not np.array_equal(got, want):
+                raise SystemExit(f"PARITY FAILURE at {e} dB {prof} frames {idx.tolist()}")
+            checked += len(idx)
+        frames += n
+    torch.cuda.synchronize()
+    f_, be, fe = ctr.tolist()
+    print(json.dumps({"code": [N, K], "design_ebn0": a.design, "ebn0": e, "profile": prof,
+                      "first_frame": a.first_frame, "frames": f_, "frame_errors": fe, "bit_errors": be,
+                      "error_frames": err_frames, "oracle_checked_frames": checked,
+                      "seconds": round(time.time() - t0, 1)}), flush=True)
+
+
 def batch(a):
     N, K = map(int, a.code.split(","))
     code = pb.PolarCode.ga(N, K, a.design)
@@ -146,7 +200,9 @@ def idud(a):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("mode", choices=["fer", "batch", "idud"])
+    ap.add_argument("mode", choices=["fer", "ferfast", "batch", "idud"])
+    ap.add_argument("--first-frame", type=int, default=0)
+    ap.add_argument("--max-seconds", type=float, default=1e9)
     ap.add_argument("--batch", type=int, default=65536)
     ap.add_argument("--code", default="32768,27568")
     ap.add_argument("--design", type=float, default=4.0)
@@ -158,4 +214,4 @@ if __name__ == "__main__":
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--max-log4", type=int, default=8)
     a = ap.parse_args()
-    {"fer": fer, "batch": batch, "idud": idud}[a.mode](a)
+    {"fer": fer, "ferfast": ferfast, "batch": batch, "idud": idud}[a.mode](a)
