@@ -283,6 +283,30 @@ def main():
             us = np.array([a.elapsed_time(b) * 1e3 for a, b in ts])
             res[prof] = {"p50_us": float(np.median(us)), "p99_us": float(np.percentile(us, 99))}
         res["n_ops"] = code.n_ops
+        # host-observed end to end (the paper's definition, copies included):
+        # host int8 frame -> info bits in host memory, wall clock per call
+        hx = llr.cpu().numpy().reshape(-1).copy()
+        hout = np.zeros(code.info_words, np.uint32)
+        hin_t = torch.from_numpy(llr.cpu().numpy()).pin_memory()
+        hout_t = torch.zeros(1, code.info_words, dtype=torch.int32).pin_memory()
+
+        def wall(fn, n=iters):
+            for _ in range(20):
+                fn()
+            t = []
+            for _ in range(n):
+                t0 = time.perf_counter_ns()
+                fn()
+                t.append((time.perf_counter_ns() - t0) / 1e3)
+            return {"p50_us": float(np.median(t)), "p99_us": float(np.percentile(t, 99))}
+
+        res["e2e_host_path_i8"] = wall(lambda: code.decode_host(hin_t, hout_t))
+        code.mailbox_open(idle_seconds=60.0)
+        try:
+            res["e2e_mailbox_i8"] = wall(lambda: code.mailbox_decode_i8(hx, hout))
+        finally:
+            code.mailbox_close()
+        assert np.array_equal(hout, hout_t.numpy().view(np.uint32)[0]), "mailbox and host path disagree"
         return res
 
     main_r = throughput(CODE, args.batch, args.steps, args.warmup, with_e2e=True)

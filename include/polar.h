@@ -85,9 +85,13 @@ polar_status polar_code_schedule(const polar_code* h, char* buf, uint32_t cap, u
 polar_status polar_code_is_specialised(const polar_code* h, int* specialised);
 
 /* Kernel variant used by the decode calls: 0 = automatic (default: the latency variant,
- * one CTA per frame, when n_frames <= number of SMs (x4 for N >= 16384), else the throughput
- * variant, one warp per frame), 1 = always throughput, 2 = always latency.  Both decode identically.  Not
- * thread-safe with concurrent decode calls on the same handle. */
+ * one CTA per frame, when n_frames <= number of SMs (x4 for N >= 16384); for int8 codes with
+ * N <= 1024 and n_frames >= 128 x number of SMs the frame-interleaved variant; else the
+ * throughput variant, one warp per frame), 1 = always throughput, 2 = always latency,
+ * 3 = the generic program-interpreted decoder, 4 = frame-interleaved (one lane per frame,
+ * int8 only; f32 calls use the throughput variant).  All decode identically (bit for bit).
+ * Returns POLAR_ERR_INVALID_ARGUMENT for any other value.  Not thread-safe with concurrent
+ * decode calls on the same handle. */
 polar_status polar_code_set_variant(polar_code* h, int variant);
 
 /* Copy the handle's frozen mask (N bytes, 1 = frozen) into host buffer mask_out. */
@@ -122,6 +126,26 @@ polar_status polar_decode_f32_host(polar_code* h, const float* host_llr, int64_t
                                    uint32_t* host_info);
 polar_status polar_decode_i8_host(polar_code* h, const int8_t* host_llr, int64_t n_frames,
                                   uint32_t* host_info);
+
+/* Batch-1 mailbox (the paper's latency includes the frame copy in and the
+ * estimate out).  polar_mailbox_open launches ONE persistent CTA running the
+ * handle's unrolled int8 latency decoder, which polls a control word in host-mapped pinned
+ * memory; it occupies one SM until polar_mailbox_close (or until idle_seconds, in (0, 3600],
+ * pass without a request, after which it exits on its own).  polar_mailbox_decode_i8 copies
+ * one frame of N int8 LLRs from host_llr (any host memory) into the mapped frame buffer,
+ * posts it, spins until the kernel has written x_hat[A] (ceil(K/32) words, same packing as
+ * polar_decode_i8) and copies it to host_info: no kernel launch, memcpy call or stream
+ * synchronisation per frame.  Blocking; not thread-safe on one handle; while the mailbox is
+ * open, a device-wide synchronisation (cudaDeviceSynchronize) would wait for the kernel to
+ * exit, so use stream synchronisation for other work on the device.
+ * Errors: POLAR_ERR_UNSUPPORTED_CODE if no mailbox kernel was built for the code (codes.txt
+ * MAILBOX=1); POLAR_ERR_INVALID_ARGUMENT for null pointers, bad idle_seconds, a second open or
+ * a decode without open; POLAR_ERR_CUDA if the kernel does not answer within timeout_seconds
+ * (it timed out idle or faulted: close and reopen); POLAR_ERR_OUT_OF_MEMORY. */
+polar_status polar_mailbox_open(polar_code* h, double idle_seconds);
+polar_status polar_mailbox_decode_i8(polar_code* h, const int8_t* host_llr, uint32_t* host_info,
+                                     double timeout_seconds);
+polar_status polar_mailbox_close(polar_code* h);
 
 /* ---------------------------------------------------------------- non-hot helpers ---- */
 

@@ -27,7 +27,8 @@ EXPORTS = [
     "polar_status_string", "polar_last_error", "polar_code_create", "polar_code_destroy",
     "polar_code_query", "polar_code_schedule", "polar_code_mask", "polar_code_set_variant",
     "polar_code_is_specialised", "polar_decode_f32",
-    "polar_decode_i8", "polar_decode_f32_host", "polar_decode_i8_host", "polar_construct_ga",
+    "polar_decode_i8", "polar_decode_f32_host", "polar_decode_i8_host", "polar_mailbox_open",
+    "polar_mailbox_decode_i8", "polar_mailbox_close", "polar_construct_ga",
     "polar_encode_systematic", "polar_gen_bpsk_awgn", "polar_count_errors",
     "polar_registry_size", "polar_registry_entry", "polar_trace_fetch",
 ]
@@ -65,6 +66,9 @@ def lib() -> C.CDLL:
         "polar_decode_i8": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
         "polar_decode_f32_host": (C.c_int, [vp, vp, C.c_int64, vp]),
         "polar_decode_i8_host": (C.c_int, [vp, vp, C.c_int64, vp]),
+        "polar_mailbox_open": (C.c_int, [vp, C.c_double]),
+        "polar_mailbox_decode_i8": (C.c_int, [vp, vp, vp, C.c_double]),
+        "polar_mailbox_close": (C.c_int, [vp]),
         "polar_construct_ga": (C.c_int, [C.c_uint32, C.c_uint32, C.c_double, vp]),
         "polar_encode_systematic": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
         "polar_gen_bpsk_awgn": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_int64, C.c_double, C.c_float,
@@ -202,6 +206,19 @@ class PolarCode:
         fn = lib().polar_decode_i8_host if is_i8 else lib().polar_decode_f32_host
         _check(fn(self._h, _ptr(llr), n, _ptr(out)))
         return out
+
+    # ------------------------------------------------------------ batch-1 mailbox (N3)
+    def mailbox_open(self, idle_seconds: float = 30.0) -> None:
+        """Start the persistent batch-1 decoder (polar_mailbox_open): one SM, until mailbox_close."""
+        _check(lib().polar_mailbox_open(self._h, float(idle_seconds)))
+
+    def mailbox_decode_i8(self, llr, out, timeout_seconds: float = 1.0):
+        """One frame: host int8 LLRs [N] (numpy or CPU tensor) -> host packed info bits [words]."""
+        _check(lib().polar_mailbox_decode_i8(self._h, _ptr(llr), _ptr(out), float(timeout_seconds)))
+        return out
+
+    def mailbox_close(self) -> None:
+        _check(lib().polar_mailbox_close(self._h))
 
     # ----------------------------------------------------------------- non-hot helpers
     def encode_systematic(self, info, out=None, stream=None):

@@ -56,6 +56,7 @@ struct Spec {
     int xsm = 48 * 1024;  // frame-interleaved variant: shared-memory budget per warp (XSM=; 24K/48K/72K
                           // measured 162/262/207 Gbps at (2048,1723), profiles/r1_history.md)
     int xwpc = 1;         // frame-interleaved variant: warps per CTA (XWPC=)
+    bool mailbox = false; // batch-1 persistent mailbox kernel of the int8 latency variant (MAILBOX=1)
 };
 
 // Distinct small-subtree patterns emitted once as __noinline__ device functions, so that the
@@ -817,6 +818,15 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                  << "extern const unsigned polar_smem_" << sp.name << "_xf_i8;\n"
                  << "extern const unsigned polar_gslot_" << sp.name << "_xf_i8;\n";
     }
+    const bool mbox = sp.mailbox && sp.N >= 64 && sp.N > WL;
+    if (mbox) {
+        const std::string km = "pd::k_mailbox<pd::PI8, " + CL + ", " + std::to_string(t_lat) + ">";
+        o << "extern const void* const polar_kern_" << sp.name << "_mbox_i8 = (const void*)&" << km << ";\n"
+          << "extern const unsigned polar_smem_" << sp.name << "_mbox_i8 = pd::FrameLayout<pd::PI8, " << CL << ", "
+          << t_lat << ", 1, false, false>::SMEM;\n";
+        reg_decl << "extern const void* const polar_kern_" << sp.name << "_mbox_i8;\n"
+                 << "extern const unsigned polar_smem_" << sp.name << "_mbox_i8;\n";
+    }
     std::ofstream(outdir + "/code_" + sp.name + ".cu") << o.str();
     {
         std::ofstream tl(outdir + "/trace_" + sp.name + ".txt");
@@ -840,6 +850,11 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                     << ", " << (v.lat && sp.helper && sp.N > WL ? 32 * sp.helper : 0) << "}";
     reg_entries << ", {&polar_kern_" << sp.name << "_xf_i8, &polar_smem_" << sp.name << "_xf_i8, 32, " << sp.xwpc
                 << ", 0, 0}, &polar_gslot_" << sp.name << "_xf_i8";
+    if (mbox)
+        reg_entries << ", {&polar_kern_" << sp.name << "_mbox_i8, &polar_smem_" << sp.name << "_mbox_i8, " << t_lat
+                    << ", 1, 0, 0}";
+    else
+        reg_entries << ", {nullptr, nullptr, 0, 0, 0, 0}";
     reg_entries << ", \"" << sched << "\"},\n";
 }
 
@@ -902,6 +917,7 @@ int main(int argc, char** argv) {
             else if (opt.rfind("XW=", 0) == 0) sp.xw = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("HELPER=", 0) == 0) sp.helper = std::atoi(opt.c_str() + 7);
             else if (opt.rfind("LATNI=", 0) == 0) sp.latni = std::atoi(opt.c_str() + 6) != 0;
+            else if (opt.rfind("MAILBOX=", 0) == 0) sp.mailbox = std::atoi(opt.c_str() + 8) != 0;
             else if (opt.rfind("XSM=", 0) == 0) sp.xsm = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("XWPC=", 0) == 0) sp.xwpc = std::atoi(opt.c_str() + 5);
             else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;

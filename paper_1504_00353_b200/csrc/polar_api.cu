@@ -11,6 +11,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -80,6 +81,16 @@ struct polar_code {
     uint32_t* d_stage_out[2] = {nullptr, nullptr};
     int64_t stage_frames = 0;
     size_t stage_elem = 0;
+    // batch-1 mailbox (polar_mailbox_*): host-mapped control word, frame and output
+    struct {
+        bool open = false;
+        void* ctl = nullptr;       // pd::MailboxCtl, host-mapped pinned
+        int8_t* hframe = nullptr;  // N bytes, host-mapped pinned
+        uint32_t* hout = nullptr;  // ceil(K/32) words, host-mapped pinned
+        int8_t* dbuf = nullptr;    // N bytes of device memory
+        cudaStream_t s = nullptr;
+        unsigned int seq = 0;
+    } mb;
 };
 
 static inline uint32_t words_of(uint32_t bits) { return (bits + 31) / 32; }
@@ -204,6 +215,7 @@ extern "C" polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t*
 
 extern "C" void polar_code_destroy(polar_code* h) {
     if (!h) return;
+    if (h->mb.open) polar_mailbox_close(h);
     if (h->dev_ready) {
         if (h->d_trace) cudaFree(h->d_trace);
         if (h->d_prog) cudaFree(h->d_prog);
@@ -408,6 +420,95 @@ extern "C" polar_status polar_decode_f32_host(polar_code* h, const float* host_l
 
 extern "C" polar_status polar_decode_i8_host(polar_code* h, const int8_t* host_llr, int64_t n, uint32_t* host_info) {
     return decode_host(h, true, host_llr, n, host_info);
+}
+
+// ------------------------------------------------------------- batch-1 mailbox (NEXT N3)
+struct MailboxCtlHost {  // layout of pd::MailboxCtl (kernels.cuh)
+    unsigned int req;
+    unsigned int pad0[31];
+    unsigned int done;
+    unsigned int pad1[31];
+};
+
+static void mailbox_free(polar_code* h) {
+    if (h->mb.s) cudaStreamDestroy(h->mb.s);
+    if (h->mb.ctl) cudaFreeHost(h->mb.ctl);
+    if (h->mb.hframe) cudaFreeHost(h->mb.hframe);
+    if (h->mb.hout) cudaFreeHost(h->mb.hout);
+    if (h->mb.dbuf) cudaFree(h->mb.dbuf);
+    h->mb.s = nullptr;
+    h->mb.ctl = nullptr;
+    h->mb.hframe = nullptr;
+    h->mb.hout = nullptr;
+    h->mb.dbuf = nullptr;
+    h->mb.open = false;
+}
+
+extern "C" polar_status polar_mailbox_open(polar_code* h, double idle_seconds) {
+    if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
+    if (!(idle_seconds > 0.0) || idle_seconds > 3600.0) return fail(POLAR_ERR_INVALID_ARGUMENT, "idle_seconds not in (0, 3600]");
+    if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device was available when the handle was created");
+    if (!h->entry || !h->entry->mbox_i8.kern) return fail(POLAR_ERR_UNSUPPORTED_CODE, "no mailbox kernel was built for this code (MAILBOX=1)");
+    std::lock_guard<std::mutex> lock(h->mu);
+    if (h->mb.open) return fail(POLAR_ERR_INVALID_ARGUMENT, "mailbox already open");
+    const Variant& v = h->entry->mbox_i8;
+    auto bail = [&](const char* what, cudaError_t e) {
+        mailbox_free(h);
+        cudaGetLastError();
+        return fail(e == cudaErrorMemoryAllocation ? POLAR_ERR_OUT_OF_MEMORY : POLAR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    };
+    cudaError_t e;
+    if ((e = cudaHostAlloc(&h->mb.ctl, sizeof(MailboxCtlHost), cudaHostAllocMapped)) != cudaSuccess) return bail("ctl", e);
+    if ((e = cudaHostAlloc((void**)&h->mb.hframe, h->N, cudaHostAllocMapped)) != cudaSuccess) return bail("frame", e);
+    if ((e = cudaHostAlloc((void**)&h->mb.hout, words_of(h->K) * 4, cudaHostAllocMapped)) != cudaSuccess) return bail("out", e);
+    if ((e = cudaMalloc((void**)&h->mb.dbuf, h->N)) != cudaSuccess) return bail("dbuf", e);
+    std::memset(h->mb.ctl, 0, sizeof(MailboxCtlHost));
+    h->mb.seq = 0;
+    if ((e = cudaStreamCreateWithFlags(&h->mb.s, cudaStreamNonBlocking)) != cudaSuccess) return bail("stream", e);
+    if ((e = cudaFuncSetAttribute(*v.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*v.smem)) != cudaSuccess)
+        return bail("smem attribute", e);
+    void *dctl, *dframe, *dout;
+    if ((e = cudaHostGetDevicePointer(&dctl, h->mb.ctl, 0)) != cudaSuccess) return bail("map ctl", e);
+    if ((e = cudaHostGetDevicePointer(&dframe, h->mb.hframe, 0)) != cudaSuccess) return bail("map frame", e);
+    if ((e = cudaHostGetDevicePointer(&dout, h->mb.hout, 0)) != cudaSuccess) return bail("map out", e);
+    unsigned long long idle_ns = (unsigned long long)(idle_seconds * 1e9);
+    const uint32_t* gtab = h->d_gtab;
+    int8_t* dbuf = h->mb.dbuf;
+    void* args[] = {&dframe, &dout, &dctl, &dbuf, (void*)&gtab, &idle_ns};
+    if ((e = cudaLaunchKernel(*v.kern, dim3(1), dim3(v.threads), args, *v.smem, h->mb.s)) != cudaSuccess) return bail("launch", e);
+    h->mb.open = true;
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_mailbox_decode_i8(polar_code* h, const int8_t* host_llr, uint32_t* host_info, double timeout_seconds) {
+    if (!h || !host_llr || !host_info) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
+    if (!h->mb.open) return fail(POLAR_ERR_INVALID_ARGUMENT, "mailbox not open");
+    std::memcpy(h->mb.hframe, host_llr, h->N);
+    volatile MailboxCtlHost* ctl = (volatile MailboxCtlHost*)h->mb.ctl;
+    const unsigned int seq = ++h->mb.seq;
+    __atomic_store_n(&((MailboxCtlHost*)h->mb.ctl)->req, seq, __ATOMIC_RELEASE);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint32_t spin = 0;; ++spin) {
+        if (__atomic_load_n(&((MailboxCtlHost*)h->mb.ctl)->done, __ATOMIC_ACQUIRE) == seq) break;
+        if ((spin & 1023u) == 0 &&
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_seconds) {
+            (void)ctl;
+            return fail(POLAR_ERR_CUDA, "mailbox kernel did not answer within %.3f s (idle timeout or fault)", timeout_seconds);
+        }
+    }
+    std::memcpy(host_info, h->mb.hout, words_of(h->K) * 4);
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_mailbox_close(polar_code* h) {
+    if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
+    std::lock_guard<std::mutex> lock(h->mu);
+    if (!h->mb.open) return POLAR_OK;
+    __atomic_store_n(&((MailboxCtlHost*)h->mb.ctl)->req, 0xffffffffu, __ATOMIC_RELEASE);
+    const cudaError_t e = cudaStreamSynchronize(h->mb.s);
+    mailbox_free(h);
+    if (e != cudaSuccess) return fail(POLAR_ERR_CUDA, "mailbox kernel: %s", cudaGetErrorString(e));
+    return POLAR_OK;
 }
 
 // ------------------------------------------------------------------------- construction

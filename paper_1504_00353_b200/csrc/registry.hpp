@@ -30,6 +30,7 @@ struct RegistryEntry {
     Variant lat_f32, lat_i8;  // latency: one CTA of threads per frame
     Variant xf_i8;            // frame-interleaved throughput: one lane per frame (frames = warps per CTA)
     const unsigned* xf_gslot; // its global scratch bytes per warp
+    Variant mbox_i8;          // batch-1 mailbox kernel (kern == nullptr: not built for this code)
     const char* schedule;     // ';'-separated Listing-1 op list
 };
 

@@ -275,3 +275,42 @@ def test_host_buffer_path_equals_device_path():
         pout = torch.zeros(300, code.info_words, dtype=torch.int32).pin_memory()
         code.decode_host(pinned, pout)
         np.testing.assert_array_equal(pout.numpy().view(np.uint32), host_out)
+
+
+def test_mailbox_batch1_equals_oracle_and_error_paths():
+    """Batch-1 mailbox (persistent kernel on host-mapped memory): every frame
+    bit-identical to the oracle, -128 clamped, clean close, and the documented errors."""
+    import time
+    for (N, K, e) in [(2048, 1723, 4.0), (32768, 29492, 4.5)]:
+        mask = oracle.construct_ga(N, K, e)
+        code = pb.PolarCode(N, K, mask)
+        _, _, q = frames(mask, K, 5, e - 0.5, seed=77)
+        q[0, :7] = -128
+        q[1] = random_llr_i8(78, (1, N), -2, 2)[0]  # ties
+        want = expected(mask, q)
+        out = np.zeros(code.info_words, np.uint32)
+        with pytest.raises(pb.PolarError):  # not open
+            code.mailbox_decode_i8(np.ascontiguousarray(q[0]), out)
+        code.mailbox_open(idle_seconds=30.0)
+        try:
+            with pytest.raises(pb.PolarError):  # second open
+                code.mailbox_open()
+            for _ in range(2):
+                for i in range(len(q)):
+                    out[:] = 0
+                    code.mailbox_decode_i8(np.ascontiguousarray(q[i]), out)
+                    assert np.array_equal(out, want[i]), f"mailbox ({N},{K}) frame {i}"
+        finally:
+            code.mailbox_close()
+        code.mailbox_close()  # closing twice is a no-op
+    # idle self-exit: the kernel leaves on its own; the next request times out; close still works
+    code.mailbox_open(idle_seconds=0.2)
+    time.sleep(0.6)
+    with pytest.raises(pb.PolarError) as err:
+        code.mailbox_decode_i8(np.ascontiguousarray(q[0]), out, timeout_seconds=0.2)
+    assert err.value.status == pb.POLAR_ERR_CUDA
+    code.mailbox_close()
+    other = pb.PolarCode(1024, 512, oracle.construct_ga(1024, 512, 2.5))
+    with pytest.raises(pb.PolarError) as err:
+        other.mailbox_open()
+    assert err.value.status == pb.POLAR_ERR_UNSUPPORTED_CODE
