@@ -823,7 +823,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         const std::string km = "pd::k_mailbox<pd::PI8, " + CL + ", " + std::to_string(t_lat) + ">";
         o << "extern const void* const polar_kern_" << sp.name << "_mbox_i8 = (const void*)&" << km << ";\n"
           << "extern const unsigned polar_smem_" << sp.name << "_mbox_i8 = pd::FrameLayout<pd::PI8, " << CL << ", "
-          << t_lat << ", 1, false, false>::SMEM;\n";
+          << t_lat << ", 1, true, false>::SMEM;\n";
         reg_decl << "extern const void* const polar_kern_" << sp.name << "_mbox_i8;\n"
                  << "extern const unsigned polar_smem_" << sp.name << "_mbox_i8;\n";
     }

@@ -516,24 +516,45 @@ PD_INLINE uint32_t wSPCm(const Src& s) {
 template <class P, int n, int s0, class Src>
 PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
     static_assert(n >= 64, "");
+    constexpr int J = n / 32;
     uint64_t hb = 0;
-    uint32_t best = 0xffffffffu;
-    uint32_t bj = 0;
+    uint32_t idx;
+    // balanced reductions (log2 J dependent steps instead of a J-long chain); pairing slot j
+    // with j + m/2 keeps the lower slot on equal keys, so the lowest index still wins (C10)
+    if constexpr (P::kPackedKey) {
+        uint32_t kk[J];
 #pragma unroll
-    for (int j = 0; j < n / 32; ++j) {
-        const auto x = s.v(j);
-        hb |= (uint64_t)P::hd(x) << j;
-        const uint32_t k = P::mag_key(x);
-        if (k < best) { best = k; bj = j; }
+        for (int j = 0; j < J; ++j) {
+            const auto x = s.v(j);
+            hb |= (uint64_t)P::hd(x) << j;
+            kk[j] = P::mag_key(x) | (uint32_t)(j * 32 + lane_id());
+        }
+#pragma unroll
+        for (int m = J; m > 1; m /= 2)
+#pragma unroll
+            for (int j = 0; j < m / 2; ++j) kk[j] = min(kk[j], kk[j + m / 2]);
+        idx = __reduce_min_sync(FULL, kk[0]) & 0xffffu;
+    } else {
+        uint32_t kk[J], jj[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const auto x = s.v(j);
+            hb |= (uint64_t)P::hd(x) << j;
+            kk[j] = P::mag_key(x);
+            jj[j] = j;
+        }
+#pragma unroll
+        for (int m = J; m > 1; m /= 2)
+#pragma unroll
+            for (int j = 0; j < m / 2; ++j) {
+                const bool r = kk[j + m / 2] < kk[j];
+                kk[j] = r ? kk[j + m / 2] : kk[j];
+                jj[j] = r ? jj[j + m / 2] : jj[j];
+            }
+        const uint32_t mn = __reduce_min_sync(FULL, kk[0]);
+        idx = __reduce_min_sync(FULL, kk[0] == mn ? jj[0] * 32u + lane_id() : 0xffffffffu);
     }
     const uint32_t parity = __popc(__ballot_sync(FULL, __popcll(hb) & 1)) & 1u;
-    uint32_t idx;
-    if constexpr (P::kPackedKey) {
-        idx = __reduce_min_sync(FULL, best | (bj * 32u + lane_id())) & 0xffffu;
-    } else {
-        const uint32_t mn = __reduce_min_sync(FULL, best);
-        idx = __reduce_min_sync(FULL, best == mn ? bj * 32u + lane_id() : 0xffffffffu);
-    }
     if (parity && lane_id() == (idx & 31u)) hb ^= 1ull << (idx >> 5);
     bw |= hb << s0;
 }
@@ -780,6 +801,36 @@ PD_INLINE void cRep(const TS* __restrict__ src, TSc* scratch, uint32_t* beta) {
 template <class P, int T, int n, class TS>
 PD_INLINE void cSPC(const TS* __restrict__ src, uint32_t* beta) {
     const int warp = (gtid<T>() >> 5);
+    if constexpr (P::kPackedKey) {
+        // int8: one 32-bit key (|alpha| f32 bits | index) per element, exact (see wSPCm);
+        // redux.min per warp, then over the warps
+        uint32_t best = 0xffffffffu, p = 0;
+        for (int k = warp; k < n / 32; k += T / 32) {
+            const auto x = P::ld(src[32 * k + lane_id()]);
+            const uint32_t w = __ballot_sync(FULL, P::hd(x));
+            if (lane_id() == 0) beta[k] = w;
+            p ^= __popc(w) & 1u;
+            best = min(best, P::mag_key(x) | (uint32_t)(32 * k + lane_id()));
+        }
+        best = __reduce_min_sync(FULL, best);
+        if constexpr (T > 32) {
+            __shared__ uint32_t redk[T / 32], par[T / 32];
+            if (lane_id() == 0) {
+                redk[warp] = best;
+                par[warp] = p;
+            }
+            group_sync<T>();
+            best = __reduce_min_sync(FULL, lane_id() < T / 32 ? redk[lane_id()] : 0xffffffffu);
+            p = __popc(__ballot_sync(FULL, lane_id() < T / 32 ? (par[lane_id()] & 1u) : 0u)) & 1u;
+        }
+        group_sync<T>();
+        if (gtid<T>() == 0 && p) {
+            const uint32_t idx = best & 0xffffu;
+            beta[idx >> 5] ^= 1u << (idx & 31);
+        }
+        group_sync<T>();
+        return;
+    }
     unsigned long long best = ~0ull;
     uint32_t p = 0;
     for (int k = warp; k < n / 32; k += T / 32) {

@@ -230,17 +230,21 @@ __global__ void __launch_bounds__(T, 1)
     k_mailbox(const int8_t* __restrict__ hframe, uint32_t* __restrict__ hout, MailboxCtl* ctl, int8_t* __restrict__ dbuf,
               const uint32_t* __restrict__ gtab, unsigned long long idle_ns) {
     static_assert(T > 32 && C::N % 16 == 0 && C::N >= 64, "");
-    using L = FrameLayout<P, C, T, 1, false, false>;
+    // the frame goes straight from host-mapped memory into the shared-memory channel buffer
+    // (as the TMA copy of k_frame's latency variant would put it); dbuf is unused
+    using L = FrameLayout<P, C, T, 1, true, false>;
     constexpr int N = C::N;
     extern __shared__ __align__(128) unsigned char smem_all[];
     __shared__ unsigned int s_req;
     using st_t = typename P::st_t;
-    st_t* const stages = (st_t*)smem_all;
-    typename P::v_t* const wst = (typename P::v_t*)(smem_all + L::WST_OFF);
-    uint32_t* const beta = (uint32_t*)(smem_all + L::STAGES);
-    uint32_t* const stg = (uint32_t*)(L::STG ? smem_all + L::STAGES + L::BETA : (unsigned char*)stages);
+    int8_t* const chan = (int8_t*)smem_all;
+    st_t* const stages = (st_t*)(smem_all + L::NBUF * L::BUF);
+    typename P::v_t* const wst = (typename P::v_t*)(smem_all + L::NBUF * L::BUF + L::WST_OFF);
+    uint32_t* const beta = (uint32_t*)(smem_all + L::NBUF * L::BUF + L::STAGES);
+    uint32_t* const stg = (uint32_t*)(L::STG ? smem_all + L::NBUF * L::BUF + L::STAGES + L::BETA : (unsigned char*)stages);
     const OpSync<T> sync{(uint32_t)T, nullptr, 0};
     unsigned int seq = 0;
+    (void)dbuf;
     for (;;) {
         if (threadIdx.x == 0) {
             const unsigned long long t0 = globaltimer_ns();
@@ -259,11 +263,19 @@ __global__ void __launch_bounds__(T, 1)
         const unsigned int r = s_req;
         if (r == 0xffffffffu) break;
         seq = r;
-        for (int i = threadIdx.x; i < N / 16; i += T) ((int4*)dbuf)[i] = __ldcv((const int4*)hframe + i);
+        constexpr int V = N / 16;  // 16-byte vectors of the frame; all loads of a thread first
+        constexpr int PER = (V + T - 1) / T;
+        int4 v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+            if (threadIdx.x + k * T < V) v[k] = __ldcv((const int4*)hframe + threadIdx.x + k * T);
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+            if (threadIdx.x + k * T < V) ((int4*)chan)[threadIdx.x + k * T] = v[k];
         if constexpr (C::STAGE_ELEMS > 0)
             for (int k = threadIdx.x; k < N / 32; k += T) beta[k] = 0;
         __syncthreads();
-        C::template decode<P, T, false, L::WF32, SP_GLOBAL>((const int8_t*)dbuf, stages, (st_t*)nullptr, wst, beta, sync);
+        C::template decode<P, T, false, L::WF32, SP_SHARED>((const int8_t*)chan, stages, (st_t*)nullptr, wst, beta, sync);
         sync();
         gather_info<N, C::K, T>(beta, gtab, stg, hout);
         __threadfence_system();
