@@ -519,8 +519,8 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
     constexpr int J = n / 32;
     uint64_t hb = 0;
     uint32_t idx;
-    // balanced reductions (log2 J dependent steps instead of a J-long chain); pairing slot j
-    // with j + m/2 keeps the lower slot on equal keys, so the lowest index still wins (C10)
+    // balanced reductions (log2 J dependent steps instead of a J-long chain); the lowest index
+    // among equal magnitudes still wins (C10): int8 packs the index into the key
     if constexpr (P::kPackedKey) {
         uint32_t kk[J];
 #pragma unroll
@@ -543,13 +543,15 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
             kk[j] = P::mag_key(x);
             jj[j] = j;
         }
+        // adjacent pairs (j, j + s): every slot on the left holds lower indices than its
+        // partner's, so keeping the left on equal keys keeps the lowest index
 #pragma unroll
-        for (int m = J; m > 1; m /= 2)
+        for (int st = 1; st < J; st *= 2)
 #pragma unroll
-            for (int j = 0; j < m / 2; ++j) {
-                const bool r = kk[j + m / 2] < kk[j];
-                kk[j] = r ? kk[j + m / 2] : kk[j];
-                jj[j] = r ? jj[j + m / 2] : jj[j];
+            for (int j = 0; j + st < J; j += 2 * st) {
+                const bool r = kk[j + st] < kk[j];
+                kk[j] = r ? kk[j + st] : kk[j];
+                jj[j] = r ? jj[j + st] : jj[j];
             }
         const uint32_t mn = __reduce_min_sync(FULL, kk[0]);
         idx = __reduce_min_sync(FULL, kk[0] == mn ? jj[0] * 32u + lane_id() : 0xffffffffu);
