@@ -127,3 +127,28 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(pb.PolarError) as e:
         c.decode_f32(llr, out, stream=0)
     assert e.value.status == pb.POLAR_ERR_CUDA
+
+
+def test_variant_and_mailbox_argument_checks_without_gpu():
+    """Variant selection accepts 0..4 (4 = frame-interleaved) and rejects the rest; the batch-1
+    mailbox reports a missing device or a code built without it, and never falls back to the CPU."""
+    torch = pytest.importorskip("torch")
+    c = pb.PolarCode(8, 5, np.array([1, 1, 0, 0, 1, 0, 0, 0], np.uint8))
+    for v in ("auto", "throughput", "latency", "generic", "xframe"):
+        c.set_variant(v)
+    with pytest.raises(pb.PolarError) as e:
+        pb._check(pb.lib().polar_code_set_variant(c._h, 5))
+    assert e.value.status == pb.POLAR_ERR_INVALID_ARGUMENT
+    out = np.zeros(1, np.uint32)
+    with pytest.raises(pb.PolarError) as e:  # not open
+        c.mailbox_decode_i8(np.zeros(8, np.int8), out)
+    assert e.value.status == pb.POLAR_ERR_INVALID_ARGUMENT
+    with pytest.raises(pb.PolarError) as e:
+        pb._check(pb.lib().polar_mailbox_open(c._h, 0.0))  # idle_seconds must be > 0
+    assert e.value.status == pb.POLAR_ERR_INVALID_ARGUMENT
+    c.mailbox_close()  # closing a mailbox that is not open is a no-op
+    if not torch.cuda.is_available():
+        for code in (c, pb.PolarCode.ga(2048, 1723, 4.0)):
+            with pytest.raises(pb.PolarError) as e:
+                code.mailbox_open()
+            assert e.value.status == pb.POLAR_ERR_CUDA
