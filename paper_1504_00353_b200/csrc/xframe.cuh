@@ -71,11 +71,6 @@ __host__ __device__ constexpr int space() { return S == SM ? SP_SHARED : SP_GLOB
 template <int S>
 __host__ __device__ constexpr int hint() { return S == CH ? L2_FIRST : S == GL ? L2_LAST : L2_NORMAL; }
 
-template <int S, int OFF>
-PD_INLINE void ld_chunk(Chunk<PI8, 16>& k, const Ctx& x, int c) {
-    k.template load_raw<space<S>(), hint<S>()>(cptr<S, OFF>(x, c));
-}
-
 
 // ------------------------------------------------------------- stage -> stage operations
 // F<n> (eq:f), G<n> (eq:g with the left child's beta), G_0R<n>:
