@@ -17,7 +17,7 @@
 //    w*32 + l;
 //  * nodes of N_v <= 32 run on f32 registers holding the integers (lF/lG/lR1/lRep/lSPC of
 //    decoder.cuh: exact, same op order as the oracle); stage ops on N_v >= 64 compute in
-//    integer-valued f16x2 (Chunk<PI8, 16>, exact for |values| <= 254).
+//    integer-valued f16x2 (XChunk: exact for |values| <= 254; the stages hold x + 128).
 #pragma once
 
 #include "decoder.cuh"
@@ -80,6 +80,62 @@ __host__ __device__ constexpr int hint() { return S == CH ? L2_FIRST : S == GL ?
 // order): 2U loads in flight per lane, and each lane reads 16U contiguous bytes of the
 // frame-major channel (whole 64-byte DRAM bursts at U = 4).
 enum : int { OP_F = 0, OP_G = 1, OP_G0R = 2 };
+
+// 16 int8 LLRs of one chunk, computed as integer-valued f16x2 (exact, |values| <= 254).
+// XF_BIASED: the decoder's own stages hold x + 128 (bytes 1..255), so unpacking is one PRMT
+// and one HADD2 per pair and packing drops the sign flip; the channel stays plain int8
+// (-128 read as -127, reading C8).
+#ifndef XF_BIASED
+#define XF_BIASED 1
+#endif
+struct XChunk {
+    uint32_t w[4];
+    uint32_t h[8];
+    template <int S>
+    PD_INLINE void load(const int8_t* p) { vld<space<S>(), 16, hint<S>()>(p, w); }
+    template <int S>
+    PD_INLINE void unpack() {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t t = (S == CH || !XF_BIASED) ? w[q] ^ 0x80808080u : w[q];
+            h[2 * q] = h2add(__byte_perm(t, 0x64646464u, 0x4140), 0xE480E480u);
+            h[2 * q + 1] = h2add(__byte_perm(t, 0x64646464u, 0x4342), 0xE480E480u);
+            if constexpr (S == CH) {
+                h[2 * q] = h2max(h[2 * q], 0xD7F0D7F0u);
+                h[2 * q + 1] = h2max(h[2 * q + 1], 0xD7F0D7F0u);
+            }
+        }
+    }
+    template <int D>
+    PD_INLINE void store(int8_t* p) const {
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            o[q] = __byte_perm(h2add(h[2 * q], 0x64806480u), h2add(h[2 * q + 1], 0x64806480u), 0x6420) ^
+                   (XF_BIASED ? 0u : 0x80808080u);
+        vst<space<D>(), 16, hint<D>()>(p, o);
+    }
+    PD_INLINE void f(const XChunk& b) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) h[q] = h2minxs(h[q], b.h[q]);
+    }
+    // h = sat(b + (beta ? -h : h)); bit k of bits = beta of element k (see Chunk<PI8>::g)
+    PD_INLINE void g(const XChunk& b, uint32_t bits) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t m = (((bits >> (2 * q)) & 3u) * 0x40008000u) & 0x80008000u;
+            h[q] = h2minxs(h2add(b.h[q], h[q] ^ m), 0x57F057F0u);
+        }
+    }
+    PD_INLINE void g0(const XChunk& b) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) h[q] = h2minxs(h2add(b.h[q], h[q]), 0x57F057F0u);
+    }
+};
+// A stage word of 4 LLRs as signed bytes (for the leaves)
+template <int S>
+PD_INLINE uint32_t sbytes(uint32_t w) { return (S == CH || !XF_BIASED) ? w : w ^ 0x80808080u; }
+
 // p: the parent's chunk 0 (channel: this lane's frame; stage: its interleaved base + lane*16)
 template <int S>
 PD_INLINE const int8_t* chunk_at(const int8_t* p, int c) { return p + (S == CH ? 16 : 512) * c; }
@@ -91,14 +147,13 @@ template <int OP, int n, int S, int D>
 PD_INLINE void sOp_impl(const int8_t* p, int8_t* d, const uint32_t* bw) {
     constexpr int H = n / 32;  // chunks of the child
     constexpr int U = H < 4 ? H : 4;
-    constexpr bool CL = S == CH;
 #pragma unroll 1
     for (int c0 = 0; c0 < H; c0 += U) {
-        Chunk<PI8, 16> a[U], b[U];
+        XChunk a[U], b[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) a[u].template load_raw<space<S>(), hint<S>()>(chunk_at<S>(p, c0 + u));
+        for (int u = 0; u < U; ++u) a[u].template load<S>(chunk_at<S>(p, c0 + u));
 #pragma unroll
-        for (int u = 0; u < U; ++u) b[u].template load_raw<space<S>(), hint<S>()>(chunk_at<S>(p, c0 + u + H));
+        for (int u = 0; u < U; ++u) b[u].template load<S>(chunk_at<S>(p, c0 + u + H));
         uint32_t bits[(U + 1) / 2];
         if constexpr (OP == OP_G) {
 #pragma unroll
@@ -106,12 +161,12 @@ PD_INLINE void sOp_impl(const int8_t* p, int8_t* d, const uint32_t* bw) {
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            a[u].unpack_raw(CL);
-            b[u].unpack_raw(CL);
+            a[u].template unpack<S>();
+            b[u].template unpack<S>();
             if constexpr (OP == OP_F) a[u].f(b[u]);
             else if constexpr (OP == OP_G0R) a[u].g0(b[u]);
             else a[u].g(b[u], (bits[u / 2] >> (16 * (u & 1))) & 0xffffu);
-            a[u].template store<space<D>(), false, hint<D>()>(chunk_at<D>(d, c0 + u));
+            a[u].template store<D>(chunk_at<D>(d, c0 + u));
         }
     }
 }
@@ -143,15 +198,15 @@ PD_INLINE void h2_to_f32(const uint32_t* h, float* q) {
 }
 template <int OP, int S>
 PD_INLINE void rOp(const int8_t* p, float* q, uint32_t ml) {
-    Chunk<PI8, 16> a[2], b[2];
+    XChunk a[2], b[2];
 #pragma unroll
-    for (int c = 0; c < 2; ++c) a[c].template load_raw<space<S>(), hint<S>()>(chunk_at<S>(p, c));
+    for (int c = 0; c < 2; ++c) a[c].template load<S>(chunk_at<S>(p, c));
 #pragma unroll
-    for (int c = 0; c < 2; ++c) b[c].template load_raw<space<S>(), hint<S>()>(chunk_at<S>(p, c + 2));
+    for (int c = 0; c < 2; ++c) b[c].template load<S>(chunk_at<S>(p, c + 2));
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-        a[c].unpack_raw(S == CH);
-        b[c].unpack_raw(S == CH);
+        a[c].template unpack<S>();
+        b[c].template unpack<S>();
         if constexpr (OP == OP_F) a[c].f(b[c]);
         else if constexpr (OP == OP_G0R) a[c].g0(b[c]);
         else a[c].g(b[c], (ml >> (16 * c)) & 0xffffu);
@@ -218,7 +273,7 @@ PD_INLINE void lvR1_impl(const int8_t* p, uint32_t* bp) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) m |= hd4(w[h][q]) << (16 * h + 4 * q);
+            for (int q = 0; q < 4; ++q) m |= hd4(sbytes<S>(w[h][q])) << (16 * h + 4 * q);
         bp[32 * (c / 2)] = m;
     }
 }
@@ -234,7 +289,7 @@ PD_INLINE void lvRep_impl(const int8_t* p, uint32_t* bp) {
         vld<space<S>(), 16, hint<S>()>(chunk_at<S>(p, c), w);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const uint32_t v = S == CH ? (uint32_t)__vmaxs4(w[q], 0x81818181u) : w[q];
+            const uint32_t v = S == CH ? (uint32_t)__vmaxs4(w[q], 0x81818181u) : sbytes<S>(w[q]);
             s = __dp4a((int)v, 0x01010101, s);
         }
     }
@@ -258,8 +313,9 @@ PD_INLINE void lvSPC_impl(const int8_t* p, uint32_t* bp) {
         for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                m |= hd4(w[h][q]) << (16 * h + 4 * q);
-                const uint32_t a = __vabsss4(w[h][q]);  // |v|, -128 -> 127 (the clamp's magnitude)
+                const uint32_t sw = sbytes<S>(w[h][q]);
+                m |= hd4(sw) << (16 * h + 4 * q);
+                const uint32_t a = __vabsss4(sw);  // |v|, -128 -> 127 (the clamp's magnitude)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const uint32_t key = (((a >> (8 * j)) & 0xffu) << 16) | (uint32_t)(16 * (c + h) + 4 * q + j);
