@@ -37,7 +37,11 @@ typedef enum polar_status {
 } polar_status;
 
 /* Opaque, immutable code handle: (N, K, frozen set), its Fast-SSC tree and the
- * kernels specialised for it.  Thread-safe to share once created. */
+ * kernels specialised for it.  Thread-safe to share once created: decode calls on one handle
+ * from several threads and streams are correct (kernel variants that use the handle's global
+ * stage scratch are ordered by an event when consecutive launches come from different
+ * streams; inside a CUDA graph capture that ordering is left to the caller).  The
+ * exceptions are polar_code_set_variant and the mailbox calls, as documented there. */
 typedef struct polar_code polar_code;
 
 /* Opaque CUDA stream (cudaStream_t); NULL = the legacy default stream. */

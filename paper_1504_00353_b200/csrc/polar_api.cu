@@ -72,6 +72,12 @@ struct polar_code {
     uint16_t* d_pos = nullptr;    // K information positions, ascending (encoder / generator)
     uint32_t* d_gtab = nullptr;   // gather table: info mask words, then info-bit prefix per word
     void* d_gscratch[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // per variant global stage scratch
+    // Launches of one variant share its scratch slots: a launch on another stream waits for the
+    // previous one (event), so concurrent decode calls on one handle stay correct.
+    std::mutex sc_mu;
+    cudaEvent_t sc_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t sc_last[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool sc_used[5] = {false, false, false, false, false};
     unsigned long long* d_trace = nullptr;  // POLAR_TRACE builds: per-op clock64 of the latency variant
     uint32_t* d_info_mask = nullptr;  // N/32 words (>= 1), bit set = information position
     // host-buffer path (lazily allocated, guarded by mu)
@@ -146,6 +152,7 @@ static polar_status init_device(polar_code* h) {
         if (slot) {  // one slot per resident frame group (xf: per warp) of the persistent grid
             const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * slot;
             CUDA_TRY(cudaMalloc(&h->d_gscratch[i], bytes));
+            CUDA_TRY(cudaEventCreateWithFlags(&h->sc_ev[i], cudaEventDisableTiming));
         }
     }
     std::vector<uint16_t> pos;
@@ -222,8 +229,10 @@ extern "C" void polar_code_destroy(polar_code* h) {
         cudaFree(h->d_pos);
         cudaFree(h->d_info_mask);
         cudaFree(h->d_gtab);
-        for (int i = 0; i < 5; ++i)
+        for (int i = 0; i < 5; ++i) {
             if (h->d_gscratch[i]) cudaFree(h->d_gscratch[i]);
+            if (h->sc_ev[i]) cudaEventDestroy(h->sc_ev[i]);
+        }
         for (int i = 0; i < 2; ++i) {
             if (h->d_stage_llr[i]) cudaFree(h->d_stage_llr[i]);
             if (h->d_stage_out[i]) cudaFree(h->d_stage_out[i]);
@@ -299,6 +308,31 @@ extern "C" polar_status polar_registry_entry(uint32_t i, uint32_t* N, uint32_t* 
 
 // ------------------------------------------------------------------------- decode (hot)
 
+// Launch a kernel that uses the global scratch of variant vi, ordered after the previous
+// launch of that variant when it was on another stream.  Under stream capture the ordering is
+// the caller's (an event recorded outside the capture cannot be waited on inside it).
+static polar_status launch_with_scratch(const polar_code* hc, int vi, const void* kern, dim3 grid, dim3 block,
+                                        void** args, unsigned smem, cudaStream_t s) {
+    polar_code* h = const_cast<polar_code*>(hc);
+    if (!h->d_gscratch[vi]) {
+        CUDA_TRY(cudaLaunchKernel(kern, grid, block, args, smem, s));
+        return POLAR_OK;
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+    if (cs != cudaStreamCaptureStatusNone) {
+        CUDA_TRY(cudaLaunchKernel(kern, grid, block, args, smem, s));
+        return POLAR_OK;
+    }
+    std::lock_guard<std::mutex> lock(h->sc_mu);
+    if (h->sc_used[vi] && h->sc_last[vi] != s) CUDA_TRY(cudaStreamWaitEvent(s, h->sc_ev[vi], 0));
+    CUDA_TRY(cudaLaunchKernel(kern, grid, block, args, smem, s));
+    CUDA_TRY(cudaEventRecord(h->sc_ev[vi], s));
+    h->sc_last[vi] = s;
+    h->sc_used[vi] = true;
+    return POLAR_OK;
+}
+
 static polar_status launch_decode(const polar_code* h, bool i8, const void* llr, int64_t n, uint32_t* out,
                                   cudaStream_t s) {
     if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
@@ -339,8 +373,7 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
         const uint32_t* gtab = h->d_gtab;
         void* gs = h->d_gscratch[4];
         void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs};
-        CUDA_TRY(cudaLaunchKernel(*v.kern, dim3(grid), dim3(32 * v.frames), args, *v.smem, s));
-        return POLAR_OK;
+        return launch_with_scratch(h, 4, *v.kern, dim3(grid), dim3(32 * v.frames), args, *v.smem, s);
     }
     const bool lat = h->variant == 2 || (h->variant == 0 && n <= lat_max);
     const int vi = (lat ? 2 : 0) + (i8 ? 1 : 0);
@@ -356,8 +389,7 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     if (lat) gs = h->d_trace;
 #endif
     void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs};
-    CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(v.threads * v.frames + v.extra), args, smem, s));
-    return POLAR_OK;
+    return launch_with_scratch(h, vi, kern, dim3(grid), dim3(v.threads * v.frames + v.extra), args, smem, s);
 }
 
 extern "C" polar_status polar_decode_f32(const polar_code* h, const float* llr, int64_t n, uint32_t* info,

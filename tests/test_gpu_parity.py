@@ -314,3 +314,27 @@ def test_mailbox_batch1_equals_oracle_and_error_paths():
     with pytest.raises(pb.PolarError) as err:
         other.mailbox_open()
     assert err.value.status == pb.POLAR_ERR_UNSUPPORTED_CODE
+
+
+def test_concurrent_streams_share_a_handle():
+    """Two streams decode different frames on ONE handle at the same time; small launches so
+    both kernels are resident together. The variants with per-handle global stage scratch
+    (N = 32768 throughput, frame-interleaved) must still be exact."""
+    for (N, K, e, n, variant) in [(32768, 29492, 4.5, 300, "throughput"), (2048, 1723, 4.0, 4096, "xframe")]:
+        mask = oracle.construct_ga(N, K, e)
+        code = pb.PolarCode(N, K, mask)
+        code.set_variant(variant)
+        xs = [torch.from_numpy(random_llr_i8(90 + k, (n, N), -30, 30)).cuda() for k in range(2)]
+        want = [code.decode_i8(x) for x in xs]
+        torch.cuda.synchronize()
+        streams = [torch.cuda.Stream() for _ in range(2)]
+        outs = [torch.empty_like(w) for w in want]
+        for _ in range(20):
+            for k in range(2):
+                with torch.cuda.stream(streams[k]):
+                    code.decode_i8(xs[k], outs[k], stream=streams[k])
+            torch.cuda.synchronize()
+            for k in range(2):
+                assert torch.equal(outs[k], want[k]), f"({N},{K}) {variant} stream {k}"
+        sample = xs[0][:8].cpu().numpy()
+        assert_same(want[0][:8].cpu().numpy().view(np.uint32), expected(mask, sample), f"({N},{K}) {variant}")
