@@ -365,6 +365,16 @@ def main():
         line["cpu_baseline"] = {"value": r / 1e9, "unit": "Gbps", "cores": cores, "kind": "oracle",
                                 "sample": f"{n} frame decodes of ({N},{K}) int8 (a 2048-frame tile of 64 seeded "
                                           f"AWGN frames, repeated for >= 10 s), {dt:.1f} s on {cores} threads"}
+        # the paper's one-core protocol: the same oracle on one thread
+        r1, n1, dt1 = cpu_oracle_rate(N, K, CODE[2], 64, 1, min_seconds=4.0)
+        model = ""
+        try:
+            model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+        except (OSError, StopIteration):
+            pass
+        line["cpu_baseline"]["single_thread"] = {"value": r1 / 1e9, "unit": "Gbps", "us_per_frame": dt1 / n1 * 1e6,
+                                                 "frames": n1, "seconds": round(dt1, 1)}
+        line["cpu_baseline"]["cpu_model"] = model
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:
