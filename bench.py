@@ -282,6 +282,30 @@ def main():
             torch.cuda.synchronize()
             us = np.array([a.elapsed_time(b) * 1e3 for a, b in ts])
             res[prof] = {"p50_us": float(np.median(us)), "p99_us": float(np.percentile(us, 99))}
+            # device latency without host submission gaps: 100 single-frame decode calls in one
+            # CUDA graph (each still one full kernel launch), replayed; median of 5 replays / 100
+            gs = torch.cuda.Stream(device=dev)
+            gs.wait_stream(stream)
+            with torch.cuda.stream(gs):
+                for _ in range(3):
+                    fn(x, out)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=gs):
+                for _ in range(100):
+                    fn(x, out)
+            g.replay()
+            torch.cuda.synchronize()
+            reps = []
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                g.replay()
+                b.record(stream)
+                torch.cuda.synchronize()
+                reps.append(a.elapsed_time(b) * 1e3 / 100)
+            res[prof]["graph_us"] = float(np.median(reps))
+            del g
         res["n_ops"] = code.n_ops
         # host-observed end to end (the paper's definition, copies included):
         # host int8 frame -> info bits in host memory, wall clock per call
