@@ -903,6 +903,9 @@ PD_INLINE uint32_t pext32(uint32_t x, uint32_t m) {
     return r;
 }
 
+#ifndef POLAR_GATHER_U
+#define POLAR_GATHER_U 4  // measured: 1 -> 4 = +1.4% at (32768,29492), +1.0% at (2048,1723)
+#endif
 template <int N, int K, int T>
 PD_INLINE void gather_info(const uint32_t* beta, const uint32_t* __restrict__ tab, uint32_t* stg,
                            uint32_t* __restrict__ out) {
@@ -910,14 +913,25 @@ PD_INLINE void gather_info(const uint32_t* beta, const uint32_t* __restrict__ ta
     constexpr int NWK = (K + 31) / 32;
     for (int q = gtid<T>(); q < NWK; q += T) stg[q] = 0;
     group_sync<T>();
-    for (int k = gtid<T>(); k < NB; k += T) {
-        const uint32_t m = __ldg(tab + k);
-        if (!m) continue;
-        const uint32_t p = __ldg(tab + NB + k);
-        const uint32_t r = pext32(beta[k], m);
-        const uint32_t sh = p & 31;
-        atomicOr(stg + (p >> 5), r << sh);
-        if (sh && sh + __popc(m) > 32) atomicOr(stg + (p >> 5) + 1, r >> (32 - sh));
+    // the table loads of GU words are issued before any is used (the table lives in L2)
+    constexpr int GU = POLAR_GATHER_U;
+    for (int k0 = gtid<T>(); k0 < NB; k0 += GU * T) {
+        uint32_t m[GU], p[GU], w[GU];
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+            const int k = k0 + u * T;
+            m[u] = k < NB ? __ldg(tab + k) : 0u;
+            p[u] = k < NB ? __ldg(tab + NB + k) : 0u;
+            w[u] = k < NB ? beta[k] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < GU; ++u) {
+            if (!m[u]) continue;
+            const uint32_t r = pext32(w[u], m[u]);
+            const uint32_t sh = p[u] & 31;
+            atomicOr(stg + (p[u] >> 5), r << sh);
+            if (sh && sh + __popc(m[u]) > 32) atomicOr(stg + (p[u] >> 5) + 1, r >> (32 - sh));
+        }
     }
     group_sync<T>();
     for (int q = gtid<T>(); q < NWK; q += T) out[q] = stg[q];
