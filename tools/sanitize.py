@@ -1,5 +1,6 @@
 """Small decodes for compute-sanitizer runs (memcheck / racecheck / synccheck / initcheck):
-each registered code family and kernel variant (throughput, latency, generic) on a few
+each registered code family and kernel variant (throughput, latency, generic, frame-interleaved,
+and the batch-1 mailbox) on a few
 frames, checked against the oracle.   usage: compute-sanitizer --tool X python tools/sanitize.py"""
 import os
 import sys
@@ -21,7 +22,7 @@ for N, K, e in CASES:
     x = random_llr_i8(N + 1, (n, N), -60, 60)
     xs = {"i8": x, "f32": x.astype(np.float32)}
     want = {p: oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, v))) for p, v in xs.items()}
-    for variant in ("throughput", "latency", "generic"):
+    for variant in ("throughput", "latency", "generic", "xframe"):
         code.set_variant(variant)
         for prof in ("i8", "f32"):
             t = torch.from_numpy(xs[prof]).cuda()
@@ -36,4 +37,18 @@ ok = np.array_equal(code.decode_i8(torch.from_numpy(x).cuda()).cpu().numpy().vie
                     oracle.pack_bits(oracle.info_bits(m, oracle.fastssc_decode(m, x))))
 bad += not ok
 print("generic random mask:", "ok" if ok else "MISMATCH")
+# batch-1 mailbox (persistent kernel on host-mapped memory)
+for N, K, e in [(2048, 1723, 4.0), (32768, 29492, 4.5)]:
+    mask = oracle.construct_ga(N, K, e)
+    code = pb.PolarCode(N, K, mask)
+    x = random_llr_i8(N + 7, (2, N), -60, 60)
+    want = oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, x)))
+    code.mailbox_open(idle_seconds=120.0)
+    for i in range(2):
+        out = np.zeros(code.info_words, np.uint32)
+        code.mailbox_decode_i8(np.ascontiguousarray(x[i]), out, timeout_seconds=60.0)
+        ok = np.array_equal(out, want[i])
+        bad += not ok
+        print(f"({N},{K}) mailbox: {'ok' if ok else 'MISMATCH'}", flush=True)
+    code.mailbox_close()
 sys.exit(1 if bad else 0)
