@@ -259,6 +259,32 @@ def main():
         torch.cuda.empty_cache()
         return res
 
+    def graph_latency_us(fn, x, out, reps=100):
+        """Device latency without host submission gaps: `reps` single-frame decode calls in one
+        CUDA graph (each still one full kernel launch), replayed; median of 5 replays / reps."""
+        stream = torch.cuda.current_stream()
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(stream)
+        with torch.cuda.stream(gs):
+            for _ in range(3):
+                fn(x, out)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            for _ in range(reps):
+                fn(x, out)
+        g.replay()
+        torch.cuda.synchronize()
+        t = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+            t.append(a.elapsed_time(b) * 1e3 / reps)
+        return float(np.median(t))
+
     def latency_batch1(code_t, iters=300):
         N, K, e = code_t
         code = pb.PolarCode.ga(N, K, e)
@@ -282,30 +308,11 @@ def main():
             torch.cuda.synchronize()
             us = np.array([a.elapsed_time(b) * 1e3 for a, b in ts])
             res[prof] = {"p50_us": float(np.median(us)), "p99_us": float(np.percentile(us, 99))}
-            # device latency without host submission gaps: 100 single-frame decode calls in one
-            # CUDA graph (each still one full kernel launch), replayed; median of 5 replays / 100
-            gs = torch.cuda.Stream(device=dev)
-            gs.wait_stream(stream)
-            with torch.cuda.stream(gs):
-                for _ in range(3):
-                    fn(x, out)
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=gs):
-                for _ in range(100):
-                    fn(x, out)
-            g.replay()
-            torch.cuda.synchronize()
-            reps = []
-            for _ in range(5):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                g.replay()
-                b.record(stream)
-                torch.cuda.synchronize()
-                reps.append(a.elapsed_time(b) * 1e3 / 100)
-            res[prof]["graph_us"] = float(np.median(reps))
-            del g
+            try:  # auxiliary legs never cost the bench line: an error is recorded instead
+                res[prof]["graph_us"] = graph_latency_us(fn, x, out)
+            except Exception as exc:
+                res[prof]["graph_us"] = None
+                res[prof]["graph_error"] = str(exc)[:200]
         res["n_ops"] = code.n_ops
         # host-observed end to end (the paper's definition, copies included):
         # host int8 frame -> info bits in host memory, wall clock per call
@@ -324,13 +331,20 @@ def main():
                 t.append((time.perf_counter_ns() - t0) / 1e3)
             return {"p50_us": float(np.median(t)), "p99_us": float(np.percentile(t, 99))}
 
-        res["e2e_host_path_i8"] = wall(lambda: code.decode_host(hin_t, hout_t))
-        code.mailbox_open(idle_seconds=60.0)
         try:
-            res["e2e_mailbox_i8"] = wall(lambda: code.mailbox_decode_i8(hx, hout))
-        finally:
-            code.mailbox_close()
-        assert np.array_equal(hout, hout_t.numpy().view(np.uint32)[0]), "mailbox and host path disagree"
+            res["e2e_host_path_i8"] = wall(lambda: code.decode_host(hin_t, hout_t))
+        except Exception as exc:
+            res["e2e_host_path_i8"] = {"error": str(exc)[:200]}
+        try:
+            code.mailbox_open(idle_seconds=60.0)
+            try:
+                res["e2e_mailbox_i8"] = wall(lambda: code.mailbox_decode_i8(hx, hout))
+            finally:
+                code.mailbox_close()
+            if not np.array_equal(hout, hout_t.numpy().view(np.uint32)[0]):
+                res["e2e_mailbox_i8"]["error"] = "mailbox and host path disagree"
+        except Exception as exc:
+            res["e2e_mailbox_i8"] = {"error": str(exc)[:200]}
         return res
 
     main_r = throughput(CODE, args.batch, args.steps, args.warmup, with_e2e=True)
