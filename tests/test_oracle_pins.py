@@ -354,3 +354,29 @@ def test_fer_close_to_ga_prediction_and_int8_loss_small():
     assert 0.4 * pred < fer < 2.5 * pred
     fer8 = np.mean(np.any(oracle.fastssc_decode(frozen, si.quantize_i8(llr)) != x, axis=1))
     assert fer8 < 1.5 * fer + 10.0 / n
+
+
+def _alpha_bytes(N, elem, align):
+    """alpha memory of the paper's layout: log2(N)+1 contiguous stages of N, N/2, ..., 1
+    values, each stage aligned to the SIMD width (16 B SSE / 32 B AVX)."""
+    total, m = 0, N
+    while m >= 1:
+        total += -(-m * elem // align) * align
+        m //= 2
+    return total
+
+
+def test_paper_memory_closed_forms():
+    """SURVEY 8(c) pin 8: the memory figures the paper prints follow from its stated layout."""
+    # P:790: N = 32768 float decoder with AVX: 262,208 bytes including a 68-byte overhead
+    packed = (2 * 32768 - 1) * 4
+    assert _alpha_bytes(32768, 4, 32) == 262208
+    assert _alpha_bytes(32768, 4, 32) - packed == 68
+    # P:929-932 (tab:impl:tp_vs_gal): int8 AVX2 footprints 6 kB (N = 2048) and 98 kB (N = 32768):
+    # alpha (32-byte aligned int8 stages) + beta as one byte per codeword bit (decimal kB, as
+    # the 3,408 kB below): 6,272 B and 98,432 B
+    assert round((_alpha_bytes(2048, 1, 32) + 2048) / 1000) == 6
+    assert round((_alpha_bytes(32768, 1, 32) + 32768) / 1000) == 98
+    # P:1242 (tab:impl:power_vs_gal): 3,408 kB per stream on the K20c for 208 frames of the
+    # (2048,1707) float decoder = 208 x (N input LLRs + N output values) x 4 bytes
+    assert round(208 * (2048 + 2048) * 4 / 1000) == 3408
