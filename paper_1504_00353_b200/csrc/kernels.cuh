@@ -22,6 +22,12 @@ namespace pd {
 
 __host__ __device__ constexpr int align16(int x) { return (x + 15) & ~15; }
 
+#ifndef POLAR_DYN
+#define POLAR_DYN 1  // dynamic frame-group scheduling of the throughput variant with global stages
+#endif
+// bytes at the start of a throughput variant's global scratch (frame-group counter)
+constexpr int SCRATCH_HDR = 256;
+
 PD_INLINE void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -109,7 +115,16 @@ __global__ void __launch_bounds__(T * FPC + (T > 32 ? 32 * C::HELPER : 0), MINB)
     in_t* const buf1 = (in_t*)(smem + (DBL ? L::BUF : 0));
     st_t* const stages = (st_t*)(smem + L::NBUF * L::BUF);
     typename P::v_t* const wst = (typename P::v_t*)(smem + L::NBUF * L::BUF + L::WST_OFF);
-    unsigned char* const gslot = GTOP ? (unsigned char*)gscratch + ((long long)blockIdx.x * FPC + grp) * L::GSLOT : nullptr;
+    // DYN: frame groups after the first round are handed out by an atomic counter (the first
+    // SCRATCH_HDR bytes of gscratch, zeroed by the host before each launch), so the frames in
+    // flight stay a compact window of the input; with static striding the slots drift apart
+    // over hundreds of rounds (1M frames at N = 32768: 261 vs 281 Gbps for 64 launches of 16K).
+    constexpr bool DYN = POLAR_DYN && T == 32 && GTOP && !CHAN_SMEM;
+    constexpr int HDR = (T == 32 && GTOP) ? SCRATCH_HDR : 0;
+    unsigned long long* const gctr = (unsigned long long*)gscratch;
+    __shared__ long long s_next;
+    unsigned char* const gslot =
+        GTOP ? (unsigned char*)gscratch + HDR + ((long long)blockIdx.x * FPC + grp) * L::GSLOT : nullptr;
     uint32_t* const beta = L::GB ? (uint32_t*)(gslot + L::GSTAGE_BYTES) : (uint32_t*)(smem + L::NBUF * L::BUF + L::STAGES);
     uint32_t* const stg = (uint32_t*)(L::STG ? smem + L::NBUF * L::BUF + L::STAGES + L::BETA : (unsigned char*)stages);
     uint64_t* const bar = (uint64_t*)(smem + L::NBUF * L::BUF + L::STAGES + L::BETA + L::STG);
@@ -149,7 +164,7 @@ __global__ void __launch_bounds__(T * FPC + (T > 32 ? 32 * C::HELPER : 0), MINB)
         __syncwarp();
         if constexpr (T > 32) group_sync<T>();
     }
-    for (int it = 0; f < n_frames; f += stride, ++it) {
+    for (int it = 0; f < n_frames; ++it) {
         // warps of this round that have a frame: they alone take part in the op barriers
         const long long base = f - grp;
         const long long nf = f + stride;
@@ -195,6 +210,13 @@ __global__ void __launch_bounds__(T * FPC + (T > 32 ? 32 * C::HELPER : 0), MINB)
                 fence_proxy_async();
                 tma_load_1d(buf0, llr + nf * N, L::FRAME_BYTES, bar);
             }
+        }
+        if constexpr (DYN) {
+            if (threadIdx.x == 0) s_next = ((long long)gridDim.x + (long long)atomicAdd(gctr, 1ull)) * FPC;
+            sync();
+            f = s_next + grp;
+        } else {
+            f += stride;
         }
     }
 }

@@ -101,6 +101,13 @@ struct polar_code {
 
 static inline uint32_t words_of(uint32_t bits) { return (bits + 31) / 32; }
 
+// Must match kernels.cuh: SCRATCH_HDR bytes at the start of a throughput variant's global
+// scratch hold its frame-group counter (POLAR_DYN scheduling).
+#ifndef POLAR_DYN
+#define POLAR_DYN 1
+#endif
+constexpr size_t kScratchHdr = 256;
+
 extern "C" const char* polar_status_string(polar_status s) {
     switch (s) {
         case POLAR_OK: return "ok";
@@ -150,7 +157,7 @@ static polar_status init_device(polar_code* h) {
         if (h->occ[i] < 1) return fail(POLAR_ERR_CUDA, "decoder kernel variant %d cannot be resident", i);
         const size_t slot = i == 4 ? *e->xf_gslot : vs[i]->gscratch;
         if (slot) {  // one slot per resident frame group (xf: per warp) of the persistent grid
-            const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * slot;
+            const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * slot + (i < 2 ? kScratchHdr : 0);
             CUDA_TRY(cudaMalloc(&h->d_gscratch[i], bytes));
             CUDA_TRY(cudaEventCreateWithFlags(&h->sc_ev[i], cudaEventDisableTiming));
         }
@@ -318,14 +325,18 @@ static polar_status launch_with_scratch(const polar_code* hc, int vi, const void
         CUDA_TRY(cudaLaunchKernel(kern, grid, block, args, smem, s));
         return POLAR_OK;
     }
+    // throughput variants with global stages: zero the frame-group counter (kernels.cuh DYN)
+    const bool ctr = POLAR_DYN && vi < 2;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CUDA_TRY(cudaStreamIsCapturing(s, &cs));
     if (cs != cudaStreamCaptureStatusNone) {
+        if (ctr) CUDA_TRY(cudaMemsetAsync(h->d_gscratch[vi], 0, sizeof(unsigned long long), s));
         CUDA_TRY(cudaLaunchKernel(kern, grid, block, args, smem, s));
         return POLAR_OK;
     }
     std::lock_guard<std::mutex> lock(h->sc_mu);
     if (h->sc_used[vi] && h->sc_last[vi] != s) CUDA_TRY(cudaStreamWaitEvent(s, h->sc_ev[vi], 0));
+    if (ctr) CUDA_TRY(cudaMemsetAsync(h->d_gscratch[vi], 0, sizeof(unsigned long long), s));
     CUDA_TRY(cudaLaunchKernel(kern, grid, block, args, smem, s));
     CUDA_TRY(cudaEventRecord(h->sc_ev[vi], s));
     h->sc_last[vi] = s;
