@@ -338,3 +338,26 @@ def test_concurrent_streams_share_a_handle():
                 assert torch.equal(outs[k], want[k]), f"({N},{K}) {variant} stream {k}"
         sample = xs[0][:8].cpu().numpy()
         assert_same(want[0][:8].cpu().numpy().view(np.uint32), expected(mask, sample), f"({N},{K}) {variant}")
+
+
+def test_dynamic_frame_scheduling_many_rounds():
+    """The throughput variant of N = 32768 hands out frame groups with an atomic counter
+    (kernels.cuh DYN): ~8 rounds of the persistent grid, a ragged last group, and a second
+    launch on the same handle (the counter is re-zeroed) must equal the latency variant (no
+    dynamic scheduling) on every frame; a sample is checked against the oracle."""
+    mask = oracle.construct_ga(32768, 29492, 4.5)
+    code = pb.PolarCode(32768, 29492, mask)
+    n = 20011
+    llr = torch.empty(n, 32768, dtype=torch.int8, device="cuda")
+    code.gen_bpsk_awgn(4242, 0, n, 4.0, 4.0, llr_i8=llr)
+    code.set_variant("throughput")
+    a = code.decode_i8(llr)
+    b = code.decode_i8(llr[: n - 5000])
+    code.set_variant("latency")
+    c = code.decode_i8(llr)
+    torch.cuda.synchronize()
+    assert torch.equal(a, c), int((a != c).any(dim=1).sum())
+    assert torch.equal(b, c[: n - 5000])
+    idx = np.array([0, 1, 2665, 5329, n - 1])
+    sample = llr[torch.from_numpy(idx).cuda()].cpu().numpy()
+    assert_same(a.cpu().numpy().view(np.uint32)[idx], expected(mask, sample), "dynamic scheduling")
