@@ -156,8 +156,9 @@ static polar_status init_device(polar_code* h) {
             &h->occ[i], k, (int)(vs[i]->threads * vs[i]->frames + vs[i]->extra), *vs[i]->smem));
         if (h->occ[i] < 1) return fail(POLAR_ERR_CUDA, "decoder kernel variant %d cannot be resident", i);
         const size_t slot = i == 4 ? *e->xf_gslot : vs[i]->gscratch;
-        if (slot) {  // one slot per resident frame group (xf: per warp) of the persistent grid
-            const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * slot + (i < 2 ? kScratchHdr : 0);
+        if (slot || i == 4) {  // one slot per resident frame group (xf: per warp) of the persistent grid,
+                               // after the counter header (always present for the xf variant)
+            const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * slot + (i < 2 || i == 4 ? kScratchHdr : 0);
             CUDA_TRY(cudaMalloc(&h->d_gscratch[i], bytes));
             CUDA_TRY(cudaEventCreateWithFlags(&h->sc_ev[i], cudaEventDisableTiming));
         }
@@ -326,7 +327,7 @@ static polar_status launch_with_scratch(const polar_code* hc, int vi, const void
         return POLAR_OK;
     }
     // throughput variants with global stages: zero the frame-group counter (kernels.cuh DYN)
-    const bool ctr = POLAR_DYN && vi < 2;
+    const bool ctr = (POLAR_DYN && vi < 2) || vi == 4;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     CUDA_TRY(cudaStreamIsCapturing(s, &cs));
     if (cs != cudaStreamCaptureStatusNone) {

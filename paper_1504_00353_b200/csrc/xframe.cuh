@@ -392,19 +392,27 @@ __global__ void __launch_bounds__(32 * WPC, MINB)
     const int8_t* llr = (const int8_t*)llr_;
     unsigned char* const sw = smem_all + w * C::SMEM_WARP;
     const long long slot = (long long)blockIdx.x * WPC + w;
-    unsigned char* const gw = (unsigned char*)gscratch + slot * C::GSLOT;
+    // gscratch: a 256-byte header holding the group counter (zeroed by the host before each
+    // launch), then one slot of C::GSLOT bytes per warp of the grid
+    unsigned long long* const gctr = (unsigned long long*)gscratch;
+    unsigned char* const gw = (unsigned char*)gscratch + 256 + slot * C::GSLOT;
     xf::Ctx x;
     x.sm = (int8_t*)sw + 16 * lane;
     x.gl = (int8_t*)gw + 16 * lane;
     x.beta = (C::BETA_GL ? (uint32_t*)(gw + C::GSTAGE) : (uint32_t*)(sw + C::SSTAGE)) + lane;
     constexpr int NWK = (C::K + 31) / 32;
     const long long groups = (n_frames + 31) / 32;
-    for (long long g = slot; g < groups; g += (long long)gridDim.x * WPC) {
+    // after its first group each warp takes the next one from the counter (dynamic scheduling:
+    // the groups in flight stay a compact window and the last wave balances)
+    for (long long g = slot; g < groups;) {
         const long long f = 32 * g + lane;
         const long long fc = f < n_frames ? f : n_frames - 1;
         x.chan = llr + fc * C::N;
         C::decode(x);
         if (f < n_frames) xf::gather_store<C::N, C::K>(x, gtab, out + f * NWK);
+        long long nxt = 0;
+        if (lane == 0) nxt = (long long)gridDim.x * WPC + (long long)atomicAdd(gctr, 1ull);
+        g = __shfl_sync(0xffffffffu, nxt, 0);
     }
 }
 
