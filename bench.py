@@ -38,6 +38,22 @@ BATCH = 16384                    # frames per step per GPU for N=32768 (512 MiB 
 BATCH2 = 1 << 20                 # frames per step per GPU for N=2048 (2 GiB)
 
 
+def _relaunch(argv, n):
+    """`python bench.py --gpus N` outside torchrun: start N ranks under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1) and return its exit code."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # the NCCL log shows every rank and the transport
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # ... on stderr, so stdout keeps one JSON line
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -178,7 +194,11 @@ def main():
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-extra", action="store_true", help="skip the (2048,1723) and latency legs")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: exercise the multi-rank path on one GPU)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch(sys.argv[1:], args.gpus))
     if args.impl == "reference":
         return run_reference(args)
 
@@ -189,10 +209,18 @@ def main():
     from paper_1504_00353_b200.shard import allreduce_counters, frame_range
 
     ws, rank, local = _dist()
+    if ws != args.gpus:
+        print(f"bench: WORLD_SIZE={ws} but --gpus {args.gpus}; reporting the {ws} ranks that run", file=sys.stderr)
+    # one rank per GPU; with fewer GPUs than ranks (the gloo check on a 1-GPU lease) ranks share
+    ndev = torch.cuda.device_count()
+    local = local % max(1, ndev)
     torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    if ws > 1:
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if ws > 1:
@@ -201,7 +229,7 @@ def main():
     from paper_1504_00353_b200.shard import max_over_ranks as _mor
 
     def max_over_ranks(x: float) -> float:
-        return _mor(x, dev)
+        return _mor(x, dev if args.backend == "nccl" else None)
 
     def throughput(code_t, B, steps, warmup, with_e2e, prof="i8"):
         N, K, e = code_t
@@ -236,9 +264,12 @@ def main():
         per_launch_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
         ctr = torch.zeros(3, dtype=torch.int64, device=dev)
         code.count_errors(out, truth, ctr)
+        if args.backend == "gloo":
+            ctr = ctr.cpu()
         allreduce_counters(ctr)  # the one collective of the path
         frames, bit_err, frame_err = ctr.tolist()
-        res = {"code": code, "N": N, "K": K, "B": B, "total_ms": total_ms, "ms_per_step": total_ms / steps,
+        assert frames == ws * B, f"all-reduced frame count {frames} != {ws} ranks x {B}"
+        res = {"code": code, "N": N, "K": K, "B": B, "frames": frames, "total_ms": total_ms, "ms_per_step": total_ms / steps,
                "launch_ms": per_launch_ms, "gbps": ws * B * K * steps / (total_ms * 1e-3) / 1e9,
                "fer": frame_err / max(frames, 1), "ber": bit_err / max(frames * K, 1), "clocks": clk.summary()}
         if with_e2e:
@@ -381,6 +412,8 @@ def main():
     line = {
         "metric": "info_gbps", "value": main_r["gbps"], "unit": "Gbps", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": main_r["ms_per_step"], "higher_is_better": True,
+        "ranks": {"world_size": ws, "backend": args.backend if ws > 1 else None, "devices": min(ws, ndev),
+                  "frames_allreduced_per_step": main_r["frames"]},
         "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
         "config": {"workload": f"({N},{K}) systematic polar, int8 Fast-SSC, BPSK-AWGN {CODE[2]} dB, "
                                f"{B} frames/GPU per step resident in HBM",

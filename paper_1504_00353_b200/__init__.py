@@ -179,30 +179,69 @@ class PolarCode:
         return [s for s in buf.value.decode().split(";") if s]
 
     # ----------------------------------------------------------------- hot path
+    # The C ABI takes raw pointers and cannot see a tensor's dtype, device, layout or size, so
+    # the binding checks them (a strided slice or a wrong dtype would make the kernels read or
+    # write past the buffers).
+    def _frames(self, llr, dtype, on_cuda: bool) -> int:
+        import torch
+        if isinstance(llr, np.ndarray) and not on_cuda:  # host buffers may be numpy arrays
+            if llr.dtype != np.dtype(str(dtype).replace("torch.", "")) or not llr.flags.c_contiguous:
+                raise ValueError(f"llr must be a contiguous {dtype} array")
+            llr = torch.from_numpy(llr)
+        if not isinstance(llr, torch.Tensor):
+            raise ValueError("llr must be a torch tensor")
+        if llr.dtype != dtype:
+            raise ValueError(f"llr must be {dtype}, got {llr.dtype}")
+        if llr.is_cuda != on_cuda:
+            raise ValueError(f"llr must be a {'CUDA' if on_cuda else 'host'} tensor")
+        if not llr.is_contiguous():
+            raise ValueError("llr must be contiguous")
+        if llr.dim() == 2:
+            if llr.shape[1] != self.N:
+                raise ValueError(f"llr must be [n, {self.N}], got {tuple(llr.shape)}")
+            return llr.shape[0]
+        if llr.dim() == 1 and llr.numel() % self.N == 0:
+            return llr.numel() // self.N
+        raise ValueError(f"llr must be [n, {self.N}] (or a flat multiple of N), got {tuple(llr.shape)}")
+
     def _out(self, n: int, out, device):
+        import torch
+        if isinstance(out, np.ndarray) and device.type == "cpu":
+            if out.dtype not in (np.uint32, np.int32) or not out.flags.c_contiguous or out.size < n * self.info_words:
+                raise ValueError(f"out must be a contiguous 32-bit array of [n={n}, {self.info_words}] words")
+            return out
         if out is None:
-            import torch
-            out = torch.empty((n, self.info_words), dtype=torch.int32, device=device)
+            return torch.empty((n, self.info_words), dtype=torch.int32, device=device)
+        if not isinstance(out, torch.Tensor) or out.dtype != torch.int32 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous int32 tensor")
+        if out.device != device:
+            raise ValueError(f"out must be on {device}, got {out.device}")
+        if out.numel() < n * self.info_words:
+            raise ValueError(f"out must hold [n={n}, {self.info_words}] words, got {tuple(out.shape)}")
         return out
 
     def decode_f32(self, llr, out=None, stream=None):
         """Fast-SSC decode of float32 LLRs [n, N] (device) -> packed info bits [n, ceil(K/32)]."""
-        n = llr.shape[0] if llr.dim() > 1 else llr.numel() // self.N
+        import torch
+        n = self._frames(llr, torch.float32, True)
         out = self._out(n, out, llr.device)
         _check(lib().polar_decode_f32(self._h, _ptr(llr), n, _ptr(out), _stream(stream)))
         return out
 
     def decode_i8(self, llr, out=None, stream=None):
         """Fast-SSC decode of int8 LLRs [n, N] (device) -> packed info bits [n, ceil(K/32)]."""
-        n = llr.shape[0] if llr.dim() > 1 else llr.numel() // self.N
+        import torch
+        n = self._frames(llr, torch.int8, True)
         out = self._out(n, out, llr.device)
         _check(lib().polar_decode_i8(self._h, _ptr(llr), n, _ptr(out), _stream(stream)))
         return out
 
     def decode_host(self, llr, out):
         """End-to-end decode of HOST LLRs (float32 or int8 [n, N]) into HOST out [n, words]."""
+        import torch
         is_i8 = str(llr.dtype).endswith("int8")
-        n = llr.shape[0]
+        n = self._frames(llr, torch.int8 if is_i8 else torch.float32, False)
+        self._out(n, out, torch.device("cpu"))
         fn = lib().polar_decode_i8_host if is_i8 else lib().polar_decode_f32_host
         _check(fn(self._h, _ptr(llr), n, _ptr(out)))
         return out

@@ -72,6 +72,7 @@ struct polar_code {
     uint16_t* d_pos = nullptr;    // K information positions, ascending (encoder / generator)
     uint32_t* d_gtab = nullptr;   // gather table: info mask words, then info-bit prefix per word
     void* d_gscratch[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // per variant global stage scratch
+    size_t sc_bytes[5] = {0, 0, 0, 0, 0};  // its size (0: the variant needs none)
     // Launches of one variant share its scratch slots: a launch on another stream waits for the
     // previous one (event), so concurrent decode calls on one handle stay correct.
     std::mutex sc_mu;
@@ -155,13 +156,15 @@ static polar_status init_device(polar_code* h) {
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &h->occ[i], k, (int)(vs[i]->threads * vs[i]->frames + vs[i]->extra), *vs[i]->smem));
         if (h->occ[i] < 1) return fail(POLAR_ERR_CUDA, "decoder kernel variant %d cannot be resident", i);
+        // one slot per resident frame group (xf: per warp) of the persistent grid, after the
+        // counter header (always present for the xf variant).  The frame-interleaved scratch
+        // (~1.2 GB at N = 32768, where auto never selects it) is allocated on its first launch.
+        h->sc_bytes[i] = 0;
         const size_t slot = i == 4 ? *e->xf_gslot : vs[i]->gscratch;
-        if (slot || i == 4) {  // one slot per resident frame group (xf: per warp) of the persistent grid,
-                               // after the counter header (always present for the xf variant)
-            const size_t bytes = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * slot + (i < 2 || i == 4 ? kScratchHdr : 0);
-            CUDA_TRY(cudaMalloc(&h->d_gscratch[i], bytes));
-            CUDA_TRY(cudaEventCreateWithFlags(&h->sc_ev[i], cudaEventDisableTiming));
-        }
+        if (slot || i == 4)
+            h->sc_bytes[i] = (size_t)h->occ[i] * h->n_sm * vs[i]->frames * slot + (i < 2 || i == 4 ? kScratchHdr : 0);
+        if (h->sc_bytes[i] && i != 4) CUDA_TRY(cudaMalloc(&h->d_gscratch[i], h->sc_bytes[i]));
+        if (h->sc_bytes[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->sc_ev[i], cudaEventDisableTiming));
     }
     std::vector<uint16_t> pos;
     std::vector<uint32_t> im(std::max<uint32_t>(1, h->N / 32), 0);
@@ -231,21 +234,21 @@ extern "C" polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t*
 extern "C" void polar_code_destroy(polar_code* h) {
     if (!h) return;
     if (h->mb.open) polar_mailbox_close(h);
-    if (h->dev_ready) {
-        if (h->d_trace) cudaFree(h->d_trace);
-        if (h->d_prog) cudaFree(h->d_prog);
-        cudaFree(h->d_pos);
-        cudaFree(h->d_info_mask);
-        cudaFree(h->d_gtab);
-        for (int i = 0; i < 5; ++i) {
-            if (h->d_gscratch[i]) cudaFree(h->d_gscratch[i]);
-            if (h->sc_ev[i]) cudaEventDestroy(h->sc_ev[i]);
-        }
-        for (int i = 0; i < 2; ++i) {
-            if (h->d_stage_llr[i]) cudaFree(h->d_stage_llr[i]);
-            if (h->d_stage_out[i]) cudaFree(h->d_stage_out[i]);
-            if (h->streams[i]) cudaStreamDestroy(h->streams[i]);
-        }
+    // every resource that exists is released, also after a partial init_device (cudaFree(nullptr)
+    // is a no-op; the pointers start null)
+    if (h->d_trace) cudaFree(h->d_trace);
+    if (h->d_prog) cudaFree(h->d_prog);
+    if (h->d_pos) cudaFree(h->d_pos);
+    if (h->d_info_mask) cudaFree(h->d_info_mask);
+    if (h->d_gtab) cudaFree(h->d_gtab);
+    for (int i = 0; i < 5; ++i) {
+        if (h->d_gscratch[i]) cudaFree(h->d_gscratch[i]);
+        if (h->sc_ev[i]) cudaEventDestroy(h->sc_ev[i]);
+    }
+    for (int i = 0; i < 2; ++i) {
+        if (h->d_stage_llr[i]) cudaFree(h->d_stage_llr[i]);
+        if (h->d_stage_out[i]) cudaFree(h->d_stage_out[i]);
+        if (h->streams[i]) cudaStreamDestroy(h->streams[i]);
     }
     delete h;
 }
@@ -322,10 +325,15 @@ extern "C" polar_status polar_registry_entry(uint32_t i, uint32_t* N, uint32_t* 
 static polar_status launch_with_scratch(const polar_code* hc, int vi, const void* kern, dim3 grid, dim3 block,
                                         void** args, unsigned smem, cudaStream_t s) {
     polar_code* h = const_cast<polar_code*>(hc);
-    if (!h->d_gscratch[vi]) {
+    if (!h->sc_bytes[vi]) {
         CUDA_TRY(cudaLaunchKernel(kern, grid, block, args, smem, s));
         return POLAR_OK;
     }
+    if (!h->d_gscratch[vi]) {  // lazily allocated scratch (frame-interleaved variant)
+        std::lock_guard<std::mutex> lock(h->sc_mu);
+        if (!h->d_gscratch[vi]) CUDA_TRY(cudaMalloc(&h->d_gscratch[vi], h->sc_bytes[vi]));
+    }
+    args[4] = (void*)&h->d_gscratch[vi];
     // throughput variants with global stages: zero the frame-group counter (kernels.cuh DYN)
     const bool ctr = (POLAR_DYN && vi < 2) || vi == 4;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -529,7 +537,9 @@ extern "C" polar_status polar_mailbox_decode_i8(polar_code* h, const int8_t* hos
     if (!h->mb.open) return fail(POLAR_ERR_INVALID_ARGUMENT, "mailbox not open");
     std::memcpy(h->mb.hframe, host_llr, h->N);
     volatile MailboxCtlHost* ctl = (volatile MailboxCtlHost*)h->mb.ctl;
-    const unsigned int seq = ++h->mb.seq;
+    // 0 is the initial value of done and 0xffffffff the stop request: the sequence skips both
+    if (++h->mb.seq == 0xffffffffu) h->mb.seq = 1;
+    const unsigned int seq = h->mb.seq;
     __atomic_store_n(&((MailboxCtlHost*)h->mb.ctl)->req, seq, __ATOMIC_RELEASE);
     const auto t0 = std::chrono::steady_clock::now();
     for (uint32_t spin = 0;; ++spin) {

@@ -124,9 +124,28 @@ def test_no_cpu_fallback_without_gpu():
     c = pb.PolarCode(8, 5, np.array([1, 1, 0, 0, 1, 0, 0, 0], np.uint8))
     llr = torch.zeros(1, 8)
     out = torch.zeros(1, 1, dtype=torch.int32)
-    with pytest.raises(pb.PolarError) as e:
+    with pytest.raises(ValueError):  # the binding refuses host tensors for the device call
         c.decode_f32(llr, out, stream=0)
+    with pytest.raises(pb.PolarError) as e:  # the library itself has no CPU path
+        pb._check(pb.lib().polar_decode_f32(c._h, llr.data_ptr(), 1, out.data_ptr(), None))
     assert e.value.status == pb.POLAR_ERR_CUDA
+
+
+def test_binding_rejects_bad_tensors():
+    """The C ABI takes raw pointers; the binding checks dtype, device, contiguity, the frame
+    length and the output size before passing them."""
+    torch = pytest.importorskip("torch")
+    c = pb.PolarCode(8, 5, np.array([1, 1, 0, 0, 1, 0, 0, 0], np.uint8))
+    ok = torch.zeros(4, 8, dtype=torch.int8)
+    for bad in (torch.zeros(4, 8), torch.zeros(4, 16, dtype=torch.int8), torch.zeros(8, 8, dtype=torch.int8)[::2],
+                torch.zeros(3, dtype=torch.int8)):
+        with pytest.raises(ValueError):
+            c.decode_host(bad if bad.dtype == torch.int8 else bad.to(torch.float64), torch.zeros(4, 1, dtype=torch.int32))
+    for out in (torch.zeros(3, 1, dtype=torch.int32), torch.zeros(4, 1, dtype=torch.int64), np.zeros((4, 1), np.uint8)):
+        with pytest.raises(ValueError):
+            c.decode_host(ok, out)
+    with pytest.raises(ValueError):
+        c.decode_i8(ok)  # host tensor given to the device call
 
 
 def test_variant_and_mailbox_argument_checks_without_gpu():

@@ -323,16 +323,43 @@ def test_phi_inverse():
         assert oracle.lib().or_inv_log_phi(y) == pytest.approx(x, rel=1e-9)
 
 
-# Op counts of the unfused Listing-1 schedule for the GA masks (counts
-# obtained during the survey with the same GA recipe; a mismatch means a different mask).
-OP_COUNTS = [((1024, 512, 2.5), 299), ((2048, 1723, 4.0), 371),
-             ((32768, 29492, 4.5), 2607), ((32768, 27568, 4.0), 3577)]
+def test_phi_against_its_definition():
+    """Chung's two-piece phi (or_log_phi) against phi's definition as an integral,
+    phi(x) = 1 - (4 pi x)^-1/2 * int tanh(u/2) exp(-(u - x)^2 / (4x)) du (Chung et al. 2001,
+    the function the GA recursion m- = phi^-1(1 - (1 - phi(m))^2) is written in), evaluated by
+    quadrature: the approximation is within 3.5% of the exact value over [0.05, 80]; a wrong
+    constant (0.4527, 0.86, 0.0218, or the x >= 10 tail) moves it by 10% or more."""
+    from scipy.integrate import quad
+
+    def exact(x):
+        r = 40.0 * np.sqrt(x) + 5.0
+        v, _ = quad(lambda u: np.tanh(u / 2.0) * np.exp(-(u - x) ** 2 / (4.0 * x)), x - r, x + r, limit=400)
+        return 1.0 - v / np.sqrt(4.0 * np.pi * x)
+
+    for x in (0.05, 0.1, 0.3, 1.0, 2.0, 5.0, 9.9, 10.1, 15.0, 20.0, 40.0, 80.0):
+        assert np.exp(oracle.lib().or_log_phi(x)) / exact(x) == pytest.approx(1.0, abs=0.035), x
 
 
-@pytest.mark.parametrize("code,ops", OP_COUNTS)
-def test_op_counts_match_survey(code, ops):
+# Op and element counts of the unfused Listing-1 schedule for the GA masks, as written by the
+# committed oracle-only script tools/gen_op_counts.py into tests/golden/op_counts.txt (they
+# reproduce SURVEY section 8's table; a mismatch means a different mask or schedule).
+def _op_counts():
+    rows = []
+    for line in open(os.path.join(GOLD, "op_counts.txt")):
+        if line.strip() and not line.startswith("#"):
+            N, K, e, ops, f, g, leaf = line.split()
+            rows.append(((int(N), int(K), float(e)), (int(ops), int(f), int(g), int(leaf))))
+    return rows
+
+
+@pytest.mark.parametrize("code,counts", _op_counts())
+def test_op_counts_match_golden(code, counts):
+    import re
+
     N, K, ebn0 = code
-    assert len(oracle.fastssc_trace(oracle.construct_ga(N, K, ebn0))) == ops
+    ops = oracle.fastssc_trace(oracle.construct_ga(N, K, ebn0))
+    f = sum(int(n) // 2 for o, n in (re.match(r"(\w+)<(\d+)>", x).groups() for x in ops) if o == "F")
+    assert (len(ops), f) == counts[:2]
 
 
 # ------------------------------------------------------------------ statistics (weak pins)
