@@ -195,6 +195,15 @@ polar_status polar_count_errors(const polar_code* h, const uint32_t* decoded,
  * frame 0 (host buffer, n entries; labels in build/gen/trace_<code>.txt). */
 polar_status polar_trace_fetch(const polar_code* h, uint64_t* host, uint32_t n);
 
+/* Diagnostics of POLAR_DEBUG_DUMP builds only (libpolar_dump.so; otherwise
+ * POLAR_ERR_UNSUPPORTED_CODE).  Each decode of at most 8 frames by the throughput or latency
+ * variant of a specialised code appends, per frame and in the decoder's op order (Listing 1,
+ * P:644-656), every F / G / G_0R output vector (eq:f P:295-302, eq:g P:304-315) as floats
+ * (int8 profile: the integer values).  *stride = floats reserved per frame (N log2 N; unused
+ * entries are NaN); fetch copies n floats of frames 0.. of the last decode into host. */
+polar_status polar_debug_dump_stride(const polar_code* h, uint64_t* stride);
+polar_status polar_debug_dump_fetch(const polar_code* h, float* host, uint64_t n);
+
 /* Number of specialised codes compiled into this library, and the i-th one's (N, K) and
  * frozen mask (host buffer of at least N bytes; may be NULL to query N and K only). */
 uint32_t polar_registry_size(void);

@@ -58,6 +58,10 @@ def lib():
         L.or_fastssc_decode_f32.argtypes = [C.c_int, _u8p, C.c_void_p, C.c_long, C.c_void_p]
         L.or_fastssc_decode_i8.argtypes = [C.c_int, _u8p, C.c_void_p, C.c_long, C.c_void_p]
         L.or_fastssc_trace.argtypes = [C.c_int, _u8p, C.c_char_p, C.c_int]; L.or_fastssc_trace.restype = C.c_int
+        L.or_fastssc_dump_f32.argtypes = [C.c_int, _u8p, _f32p, _u8p, _f32p, C.c_long]
+        L.or_fastssc_dump_f32.restype = C.c_long
+        L.or_fastssc_dump_i8.argtypes = [C.c_int, _u8p, _i8p, _u8p, _i32p, C.c_long]
+        L.or_fastssc_dump_i8.restype = C.c_long
         L.or_ml_decode_f32.argtypes = [C.c_int, _u8p, _f32p, C.c_long, _u8p]
         L.or_rep_f32.argtypes = [C.c_int, _f32p, _u8p]
         L.or_spc_f32.argtypes = [C.c_int, _f32p, _u8p]
@@ -203,6 +207,23 @@ def fastssc_trace(frozen: np.ndarray) -> list[str]:
     lib().or_fastssc_trace(N, frozen, buf, cap)
     s = buf.value.decode()
     return [t for t in s.split(";") if t]
+
+
+def fastssc_alpha_dump(frozen: np.ndarray, llr: np.ndarray) -> np.ndarray:
+    """O2 on ONE frame; every F / G / G_0R output vector in op order, concatenated (float32 for
+    f32 input, int32 for int8 input): the intermediate LLRs of the decoder."""
+    frozen = np.ascontiguousarray(frozen, np.uint8)
+    N = frozen.shape[0]
+    x = np.ascontiguousarray(llr).reshape(N)
+    cap = N * max(1, int(np.log2(N)))
+    xhat = np.zeros(N, np.uint8)
+    if x.dtype == np.int8:
+        out = np.zeros(cap, np.int32)
+        n = lib().or_fastssc_dump_i8(N, frozen, x, xhat, out, cap)
+    else:
+        out = np.zeros(cap, np.float32)
+        n = lib().or_fastssc_dump_f32(N, frozen, x.astype(np.float32), xhat, out, cap)
+    return out[:n]
 
 
 def ml_decode(frozen: np.ndarray, llr: np.ndarray) -> np.ndarray:

@@ -297,7 +297,21 @@ typedef struct {
     char* buf;
     int cap;
     int len;
+    /* optional alpha dump: every F / G / G_0R output vector appended in op order (the
+     * intermediate LLRs the north star's float bar compares, 1e-5 relative); records only */
+    float* af;
+    int* ai;
+    long apos, acap;
 } or_trace;
+
+static void dump_f32(or_trace* tr, const float* v, int h) {
+    if (!tr || !tr->af) return;
+    for (int i = 0; i < h && tr->apos < tr->acap; ++i) tr->af[tr->apos++] = v[i];
+}
+static void dump_i8(or_trace* tr, const int* v, int h) {
+    if (!tr || !tr->ai) return;
+    for (int i = 0; i < h && tr->apos < tr->acap; ++i) tr->ai[tr->apos++] = v[i];
+}
 
 static void trace_op(or_trace* tr, const char* name, int n) {
     if (!tr || !tr->buf) return;
@@ -337,6 +351,7 @@ static void fssc_f32(int n, const uint8_t* frozen, const float* alpha, uint8_t* 
     if (left == OR_RATE0) {
         trace_op(tr, "G_0R", n);
         for (int i = 0; i < h; ++i) { beta[i] = 0; child[i] = or_g_f32(alpha[i], alpha[i + h], 0); }
+        dump_f32(tr, child, h);
         fssc_f32(h, frozen + h, child, beta + h, scratch + h, tr);
         trace_op(tr, "Combine_0R", n);
         for (int i = 0; i < h; ++i) beta[i] = beta[i + h];
@@ -344,6 +359,7 @@ static void fssc_f32(int n, const uint8_t* frozen, const float* alpha, uint8_t* 
     }
     trace_op(tr, "F", n);
     for (int i = 0; i < h; ++i) child[i] = or_f_f32(alpha[i], alpha[i + h]);
+    dump_f32(tr, child, h);
     fssc_f32(h, frozen, child, beta, scratch + h, tr);
     if (right == OR_RATE0) {
         trace_op(tr, "Combine_R0", n);
@@ -352,6 +368,7 @@ static void fssc_f32(int n, const uint8_t* frozen, const float* alpha, uint8_t* 
     }
     trace_op(tr, "G", n);
     for (int i = 0; i < h; ++i) child[i] = or_g_f32(alpha[i], alpha[i + h], beta[i]);
+    dump_f32(tr, child, h);
     fssc_f32(h, frozen + h, child, beta + h, scratch + h, tr);
     trace_op(tr, "Combine", n);
     for (int i = 0; i < h; ++i) beta[i] ^= beta[i + h];
@@ -374,6 +391,7 @@ static void fssc_i8(int n, const uint8_t* frozen, const int* alpha, uint8_t* bet
     if (left == OR_RATE0) {
         trace_op(tr, "G_0R", n);
         for (int i = 0; i < h; ++i) { beta[i] = 0; child[i] = or_g_i8(alpha[i], alpha[i + h], 0); }
+        dump_i8(tr, child, h);
         fssc_i8(h, frozen + h, child, beta + h, scratch + h, tr);
         trace_op(tr, "Combine_0R", n);
         for (int i = 0; i < h; ++i) beta[i] = beta[i + h];
@@ -381,6 +399,7 @@ static void fssc_i8(int n, const uint8_t* frozen, const int* alpha, uint8_t* bet
     }
     trace_op(tr, "F", n);
     for (int i = 0; i < h; ++i) child[i] = or_f_i8(alpha[i], alpha[i + h]);
+    dump_i8(tr, child, h);
     fssc_i8(h, frozen, child, beta, scratch + h, tr);
     if (right == OR_RATE0) {
         trace_op(tr, "Combine_R0", n);
@@ -389,6 +408,7 @@ static void fssc_i8(int n, const uint8_t* frozen, const int* alpha, uint8_t* bet
     }
     trace_op(tr, "G", n);
     for (int i = 0; i < h; ++i) child[i] = or_g_i8(alpha[i], alpha[i + h], beta[i]);
+    dump_i8(tr, child, h);
     fssc_i8(h, frozen + h, child, beta + h, scratch + h, tr);
     trace_op(tr, "Combine", n);
     for (int i = 0; i < h; ++i) beta[i] ^= beta[i + h];
@@ -419,13 +439,34 @@ int or_fastssc_trace(int N, const uint8_t* frozen, char* buf, int cap) {
     float* llr = (float*)calloc((size_t)N, sizeof(float));
     float* scratch = (float*)malloc(sizeof(float) * (size_t)N);
     uint8_t* xhat = (uint8_t*)malloc((size_t)N);
-    or_trace tr = {buf, cap, 0};
+    or_trace tr = {buf, cap, 0, NULL, NULL, 0, 0};
     if (cap > 0) buf[0] = 0;
     fssc_f32(N, frozen, llr, xhat, scratch, &tr);
     free(xhat);
     free(scratch);
     free(llr);
     return tr.len;
+}
+
+/* O2 on one frame, recording every F / G / G_0R output vector in op order (or_trace.af/ai):
+ * returns the number of values written (at most cap).  The decode itself is unchanged. */
+long or_fastssc_dump_f32(int N, const uint8_t* frozen, const float* llr, uint8_t* xhat, float* out, long cap) {
+    float* scratch = (float*)malloc(sizeof(float) * (size_t)N);
+    or_trace tr = {NULL, 0, 0, out, NULL, 0, cap};
+    fssc_f32(N, frozen, llr, xhat, scratch, &tr);
+    free(scratch);
+    return tr.apos;
+}
+
+long or_fastssc_dump_i8(int N, const uint8_t* frozen, const int8_t* llr, uint8_t* xhat, int* out, long cap) {
+    int* in = (int*)malloc(sizeof(int) * (size_t)N);
+    int* scratch = (int*)malloc(sizeof(int) * (size_t)N);
+    for (int i = 0; i < N; ++i) in[i] = ingest_i8(llr[i]);
+    or_trace tr = {NULL, 0, 0, NULL, out, 0, cap};
+    fssc_i8(N, frozen, in, xhat, scratch, &tr);
+    free(scratch);
+    free(in);
+    return tr.apos;
 }
 
 /* Standalone node decoders for unit pins (int8 versions take int8 inputs). */

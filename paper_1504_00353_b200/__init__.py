@@ -30,7 +30,8 @@ EXPORTS = [
     "polar_decode_i8", "polar_decode_f32_host", "polar_decode_i8_host", "polar_mailbox_open",
     "polar_mailbox_decode_i8", "polar_mailbox_close", "polar_construct_ga",
     "polar_encode_systematic", "polar_gen_bpsk_awgn", "polar_count_errors",
-    "polar_registry_size", "polar_registry_entry", "polar_trace_fetch",
+    "polar_registry_size", "polar_registry_entry", "polar_trace_fetch", "polar_debug_dump_stride",
+    "polar_debug_dump_fetch",
 ]
 
 
@@ -40,17 +41,26 @@ class PolarError(RuntimeError):
         self.status = status
 
 
-_lib = None
+_libs: dict[str, C.CDLL] = {}
+DUMP_LIB_PATH = os.path.join(_HERE, "libpolar_dump.so")
 
 
 def lib() -> C.CDLL:
     """Load libpolar.so (built by ``build()``); raises if it is absent."""
-    global _lib
-    if _lib is not None:
-        return _lib
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: run paper_1504_00353_b200.build.build() first")
-    L = C.CDLL(LIB_PATH)
+    return _load(LIB_PATH)
+
+
+def dump_lib() -> C.CDLL:
+    """libpolar_dump.so: the POLAR_DEBUG_DUMP build (test infrastructure: alpha-stage dumps)."""
+    return _load(DUMP_LIB_PATH)
+
+
+def _load(path: str) -> C.CDLL:
+    if path in _libs:
+        return _libs[path]
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run paper_1504_00353_b200.build.build() first")
+    L = C.CDLL(path)
     vp, u8p, u32p, i64p = C.c_void_p, C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_int64)
     sig = {
         "polar_status_string": (C.c_char_p, [C.c_int]),
@@ -76,6 +86,8 @@ def lib() -> C.CDLL:
         "polar_count_errors": (C.c_int, [vp, vp, vp, C.c_int64, vp, vp]),
         "polar_registry_size": (C.c_uint32, []),
         "polar_trace_fetch": (C.c_int, [vp, vp, C.c_uint32]),
+        "polar_debug_dump_stride": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
+        "polar_debug_dump_fetch": (C.c_int, [vp, vp, C.c_uint64]),
         "polar_registry_entry": (C.c_int, [C.c_uint32, u32p, u32p, vp]),
     }
     for name, (res, args) in sig.items():
@@ -83,13 +95,13 @@ def lib() -> C.CDLL:
         fn.restype = res
         fn.argtypes = args
     _ = (u8p, i64p)
-    _lib = L
+    _libs[path] = L
     return L
 
 
-def _check(status: int) -> None:
+def _check(status: int, L: C.CDLL | None = None) -> None:
     if status != POLAR_OK:
-        L = lib()
+        L = L or lib()
         raise PolarError(status, f"{L.polar_status_string(status).decode()}: {L.polar_last_error().decode()}")
 
 
@@ -132,20 +144,33 @@ def registry() -> list[tuple[int, int, np.ndarray]]:
 class PolarCode:
     """Handle of one (N, K, frozen set) code: ``polar_code_create`` / ``polar_code_destroy``."""
 
-    def __init__(self, N: int, K: int, frozen_mask: np.ndarray):
+    def __init__(self, N: int, K: int, frozen_mask: np.ndarray, library: C.CDLL | None = None):
+        self._L = library or lib()
         m = np.ascontiguousarray(np.asarray(frozen_mask, np.uint8))
         if m.shape != (N,):
             raise ValueError("frozen mask must have N entries")
         h = C.c_void_p()
-        _check(lib().polar_code_create(N, K, m.ctypes.data, C.byref(h)))
+        self._chk(self._L.polar_code_create(N, K, m.ctypes.data, C.byref(h)))
         self._h = h
         n, k, ops, smem, wr = (C.c_uint32() for _ in range(5))
-        _check(lib().polar_code_query(h, C.byref(n), C.byref(k), C.byref(ops), C.byref(smem), C.byref(wr)))
+        self._chk(self._L.polar_code_query(h, C.byref(n), C.byref(k), C.byref(ops), C.byref(smem), C.byref(wr)))
         self.N, self.K, self.n_ops, self.smem_bytes, self.warp_root = n.value, k.value, ops.value, smem.value, wr.value
         self.info_words = (self.K + 31) // 32
         sp = C.c_int()
-        _check(lib().polar_code_is_specialised(h, C.byref(sp)))
+        self._chk(self._L.polar_code_is_specialised(h, C.byref(sp)))
         self.specialised = bool(sp.value)
+
+    def _chk(self, status: int) -> None:
+        _check(status, self._L)
+
+    def alpha_dump(self, n_frames: int) -> np.ndarray:
+        """POLAR_DEBUG_DUMP builds: float32 [n_frames, N log2 N], every F/G/G_0R output of the
+        last decode in op order (NaN after the last one)."""
+        st = C.c_uint64()
+        self._chk(self._L.polar_debug_dump_stride(self._h, C.byref(st)))
+        out = np.empty((n_frames, st.value), np.float32)
+        self._chk(self._L.polar_debug_dump_fetch(self._h, out.ctypes.data, out.size))
+        return out
 
     @classmethod
     def ga(cls, N: int, K: int, design_ebn0_db: float) -> "PolarCode":
@@ -153,7 +178,7 @@ class PolarCode:
 
     def close(self) -> None:
         if getattr(self, "_h", None):
-            lib().polar_code_destroy(self._h)
+            self._L.polar_code_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -164,18 +189,18 @@ class PolarCode:
 
     def set_variant(self, variant: str) -> None:
         """'auto' | 'throughput' | 'latency' | 'generic' (all decode identically)."""
-        _check(lib().polar_code_set_variant(self._h, {"auto": 0, "throughput": 1, "latency": 2, "generic": 3, "xframe": 4}[variant]))
+        self._chk(self._L.polar_code_set_variant(self._h, {"auto": 0, "throughput": 1, "latency": 2, "generic": 3, "xframe": 4}[variant]))
 
     def mask(self) -> np.ndarray:
         m = np.zeros(self.N, np.uint8)
-        _check(lib().polar_code_mask(self._h, m.ctypes.data))
+        self._chk(self._L.polar_code_mask(self._h, m.ctypes.data))
         return m
 
     def schedule(self) -> list[str]:
         need = C.c_uint32()
-        _check(lib().polar_code_schedule(self._h, None, 0, C.byref(need)))
+        self._chk(self._L.polar_code_schedule(self._h, None, 0, C.byref(need)))
         buf = C.create_string_buffer(need.value)
-        _check(lib().polar_code_schedule(self._h, buf, need.value, None))
+        self._chk(self._L.polar_code_schedule(self._h, buf, need.value, None))
         return [s for s in buf.value.decode().split(";") if s]
 
     # ----------------------------------------------------------------- hot path
@@ -225,7 +250,7 @@ class PolarCode:
         import torch
         n = self._frames(llr, torch.float32, True)
         out = self._out(n, out, llr.device)
-        _check(lib().polar_decode_f32(self._h, _ptr(llr), n, _ptr(out), _stream(stream)))
+        self._chk(self._L.polar_decode_f32(self._h, _ptr(llr), n, _ptr(out), _stream(stream)))
         return out
 
     def decode_i8(self, llr, out=None, stream=None):
@@ -233,7 +258,7 @@ class PolarCode:
         import torch
         n = self._frames(llr, torch.int8, True)
         out = self._out(n, out, llr.device)
-        _check(lib().polar_decode_i8(self._h, _ptr(llr), n, _ptr(out), _stream(stream)))
+        self._chk(self._L.polar_decode_i8(self._h, _ptr(llr), n, _ptr(out), _stream(stream)))
         return out
 
     def decode_host(self, llr, out):
@@ -242,22 +267,22 @@ class PolarCode:
         is_i8 = str(llr.dtype).endswith("int8")
         n = self._frames(llr, torch.int8 if is_i8 else torch.float32, False)
         self._out(n, out, torch.device("cpu"))
-        fn = lib().polar_decode_i8_host if is_i8 else lib().polar_decode_f32_host
-        _check(fn(self._h, _ptr(llr), n, _ptr(out)))
+        fn = self._L.polar_decode_i8_host if is_i8 else self._L.polar_decode_f32_host
+        self._chk(fn(self._h, _ptr(llr), n, _ptr(out)))
         return out
 
     # ------------------------------------------------------------ batch-1 mailbox (N3)
     def mailbox_open(self, idle_seconds: float = 30.0) -> None:
         """Start the persistent batch-1 decoder (polar_mailbox_open): one SM, until mailbox_close."""
-        _check(lib().polar_mailbox_open(self._h, float(idle_seconds)))
+        self._chk(self._L.polar_mailbox_open(self._h, float(idle_seconds)))
 
     def mailbox_decode_i8(self, llr, out, timeout_seconds: float = 1.0):
         """One frame: host int8 LLRs [N] (numpy or CPU tensor) -> host packed info bits [words]."""
-        _check(lib().polar_mailbox_decode_i8(self._h, _ptr(llr), _ptr(out), float(timeout_seconds)))
+        self._chk(self._L.polar_mailbox_decode_i8(self._h, _ptr(llr), _ptr(out), float(timeout_seconds)))
         return out
 
     def mailbox_close(self) -> None:
-        _check(lib().polar_mailbox_close(self._h))
+        self._chk(self._L.polar_mailbox_close(self._h))
 
     # ----------------------------------------------------------------- non-hot helpers
     def encode_systematic(self, info, out=None, stream=None):
@@ -265,20 +290,20 @@ class PolarCode:
         n = info.shape[0]
         if out is None:
             out = torch.empty((n, max(1, self.N // 32)), dtype=torch.int32, device=info.device)
-        _check(lib().polar_encode_systematic(self._h, _ptr(info), n, _ptr(out), _stream(stream)))
+        self._chk(self._L.polar_encode_systematic(self._h, _ptr(info), n, _ptr(out), _stream(stream)))
         return out
 
     def gen_bpsk_awgn(self, seed: int, first_frame: int, n: int, ebn0_db: float, q_scale: float = 4.0,
                       llr_f32=None, llr_i8=None, info=None, stream=None):
-        _check(lib().polar_gen_bpsk_awgn(self._h, seed, first_frame, n, float(ebn0_db), float(q_scale),
+        self._chk(self._L.polar_gen_bpsk_awgn(self._h, seed, first_frame, n, float(ebn0_db), float(q_scale),
                                          _ptr(llr_f32), _ptr(llr_i8), _ptr(info), _stream(stream)))
 
     def trace(self, n: int) -> np.ndarray:
         """clock64 stamps of the latency variant's last frame (POLAR_TRACE builds only)."""
         out = np.zeros(n, np.uint64)
-        _check(lib().polar_trace_fetch(self._h, out.ctypes.data, n))
+        self._chk(self._L.polar_trace_fetch(self._h, out.ctypes.data, n))
         return out
 
     def count_errors(self, decoded, truth, counters, stream=None):
         n = decoded.shape[0]
-        _check(lib().polar_count_errors(self._h, _ptr(decoded), _ptr(truth), n, _ptr(counters), _stream(stream)))
+        self._chk(self._L.polar_count_errors(self._h, _ptr(decoded), _ptr(truth), n, _ptr(counters), _stream(stream)))

@@ -64,11 +64,13 @@ def _compile(src, obj, flags):
     return True
 
 
-def build(verbose: bool = True, jobs: int | None = None) -> str:
+def build_one(build_dir: str, lib_out: str, spec_files, extra, verbose: bool = True, jobs: int | None = None) -> str:
+    GEN, OBJ, LIB = os.path.join(build_dir, "gen"), os.path.join(build_dir, "obj"), lib_out
+    nvflags = NVFLAGS + list(extra)
     os.makedirs(GEN, exist_ok=True)
     os.makedirs(OBJ, exist_ok=True)
     # 1. the emitter
-    gen_exe = os.path.join(BUILD, "polar_codegen")
+    gen_exe = os.path.join(build_dir, "polar_codegen")
     gsrc = [os.path.join(CSRC, "codegen.cpp"), os.path.join(CSRC, "construct.cpp"), os.path.join(CSRC, "tree.hpp")]
     gstamp = gen_exe + ".sha"
     gd = _digest(gsrc)
@@ -77,9 +79,9 @@ def build(verbose: bool = True, jobs: int | None = None) -> str:
         with open(gstamp, "w") as f:
             f.write(gd)
     # 2. emit into a scratch dir, then replace only the files whose content changed
-    spec = os.path.join(BUILD, "codes_all.txt")
+    spec = os.path.join(build_dir, "codes_all.txt")
     with open(spec, "w") as f:
-        for name in SPEC_FILES:
+        for name in spec_files:
             p = name if os.path.isabs(name) else os.path.join(PKG, name)
             if os.path.exists(p):
                 f.write(open(p).read() + "\n")
@@ -106,7 +108,7 @@ def build(verbose: bool = True, jobs: int | None = None) -> str:
 
     def one(u):
         src, o = u
-        flags = NVFLAGS if src.endswith(".cu") else [f for f in NVFLAGS if f not in ("-Xptxas", "-v", "--resource-usage")]
+        flags = nvflags if src.endswith(".cu") else [f for f in nvflags if f not in ("-Xptxas", "-v", "--resource-usage")]
         t = _compile(src, os.path.join(OBJ, o), flags)
         if t and verbose:
             print(f"[polar build] compiled {os.path.basename(src)}", flush=True)
@@ -124,5 +126,20 @@ def build(verbose: bool = True, jobs: int | None = None) -> str:
     return LIB
 
 
+def build(verbose: bool = True, jobs: int | None = None) -> str:
+    """The product library (every code of codes.txt + codes_random.txt)."""
+    return build_one(BUILD, LIB, SPEC_FILES, [], verbose, jobs)
+
+
+def build_dump(verbose: bool = True, jobs: int | None = None) -> str:
+    """libpolar_dump.so: the same kernels built with POLAR_DEBUG_DUMP for the codes of
+    codes_dump.txt -- test infrastructure recording every F/G output (alpha stage) so that the
+    GPU's intermediate LLRs can be compared with the oracle's (tests/test_alpha_dump.py)."""
+    return build_one(os.path.join(PKG, "build_dump"), os.path.join(PKG, "libpolar_dump.so"), ["codes_dump.txt"],
+                     ["-DPOLAR_DEBUG_DUMP"], verbose, jobs)
+
+
 if __name__ == "__main__":
     build(jobs=int(sys.argv[1]) if len(sys.argv) > 1 else None)
+    if os.environ.get("POLAR_BUILD_DUMP", "1") != "0":
+        build_dump(jobs=int(sys.argv[1]) if len(sys.argv) > 1 else None)

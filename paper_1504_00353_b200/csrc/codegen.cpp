@@ -53,6 +53,7 @@ struct Spec {
     bool latni = false;   // latency variant: non-inlined subtree copies (LATNI=1)
     bool gbeta = false;   // throughput variant: decision bits in the global slot scratch too (GBETA=1)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
+    int h16 = 0;          // int8 throughput variant: stages of size <= h16 stored as f16 (H16=; 0: none)
     int xsm = 48 * 1024;  // frame-interleaved variant: shared-memory budget per warp (XSM=; 24K/48K/72K
                           // measured 162/262/207 Gbps at (2048,1723), profiles/r1_history.md)
     int xwpc = 1;         // frame-interleaved variant: warps per CTA (XWPC=)
@@ -310,14 +311,25 @@ struct CtaEmitter {
     SharedFns* sh = nullptr;
 
     // GTOP (template flag of decode): the largest stages live in per-frame global scratch.
-    // The stage of size W (the register subtrees' input) is kept as f32 in `wst`.
-    std::string stage(int m) {
-        if (m == W) return "@W";  // f32 `wst` in the latency variant (WF32), else an int8/f32 stage
+    // The stage of size W (the register subtrees' input) is kept as f32 in `wst` (WF32).
+    // H16 (template flag; int8 throughput variant, spec option H16=): stages of size <= h16
+    // are f16 values (the f16x2 stage ops then load and store them without conversion), laid
+    // out by byte offsets hoff (global or shared).  Statements name a stage by the placeholder
+    // @S<m>@ and its state space by @P<m>@; emit_raw writes one copy per layout.
+    int h16 = 0;
+    std::map<int, int> hoff;  // H16 layout: stage size -> byte offset (in gst or stages)
+    std::string stage(int m) { return "@S" + std::to_string(m) + "@"; }
+    std::string stage_s(int m) {  // default layout (element offsets of P::st_t)
         if (goff.count(m)) return "(GTOP ? gst + " + std::to_string(goff.at(m)) + " : stages + " + std::to_string(stage_off.at(m)) + ")";
-        return "(stages + (GTOP ? " + std::to_string(soff.at(m)) + " : " + std::to_string(stage_off.at(m)) + "))";
+        if (soff.count(m)) return "(stages + (GTOP ? " + std::to_string(soff.at(m)) + " : " + std::to_string(stage_off.at(m)) + "))";
+        return "(stages + " + std::to_string(stage_off.at(m)) + ")";
+    }
+    std::string stage_h(int m) {
+        const std::string ty = m <= h16 ? "__half" : "typename P::st_t";
+        return "((" + ty + "*)((unsigned char*)" + (goff.count(m) ? "gst" : "stages") + " + " + std::to_string(hoff.at(m)) + "))";
     }
 
-    // Emit one statement; "@W" (the stage of size W) becomes `wst` under WF32, else its slot
+    // Emit one statement; stage placeholders (stage(), space()) are resolved per layout by emit_raw.
     // in the stage arrays.
     std::string last_op;
     // Warp-0 regions (latency variant, XW): a CTA-level node of size <= XW is decoded by warp 0
@@ -344,20 +356,27 @@ struct CtaEmitter {
         emit_raw(stmt);
     }
     void emit_raw(const std::string& stmt) {
-        const size_t p = stmt.find("@W");
-        if (p == std::string::npos) {
+        if (stmt.find('@') == std::string::npos) {
             body << "        " << stmt << "\n";
             return;
         }
-        auto subst = [&](const std::string& by) {
+        // layout: 0 latency (WF32: the W stage is the f32 `wst`), 1 H16, 2 default
+        auto subst = [&](int layout) {
             std::string r = stmt;
-            for (size_t q; (q = r.find("@W")) != std::string::npos;) r.replace(q, 2, by);
+            for (size_t q; (q = r.find('@')) != std::string::npos;) {
+                const size_t e = r.find('@', q + 1);
+                const char kind = r[q + 1];
+                const int m = std::atoi(r.substr(q + 2, e - q - 2).c_str());
+                std::string by;
+                if (kind == 'S') by = layout == 0 && m == W ? "wst" : layout == 1 ? stage_h(m) : stage_s(m);
+                else by = layout == 1 ? (goff.count(m) ? "0" : "1") : (goff.count(m) ? "(GTOP ? 0 : 1)" : "1");
+                r.replace(q, e - q + 1, by);
+            }
             return r;
         };
-        const std::string slot = soff.count(W) ? "(stages + (GTOP ? " + std::to_string(soff.at(W)) + " : " +
-                                                     std::to_string(stage_off.at(W)) + "))"
-                                               : "(stages + " + std::to_string(stage_off.at(W)) + ")";
-        body << "        if constexpr (WF32) { " << subst("wst") << " } else { " << subst(slot) << " }\n";
+        body << "        if constexpr (WF32) { " << subst(0) << " }";
+        if (h16 > 0) body << " else if constexpr (H16) { " << subst(1) << " }";
+        body << " else { " << subst(2) << " }\n";
     }
 
     // The warp subtree is emitted twice when small subtrees are shared (DEDUP): with the
@@ -386,12 +405,8 @@ struct CtaEmitter {
         emit("sync();");
     }
 
-    // State space (SP_GLOBAL 0 / SP_SHARED 1) of a stage, as a C++ constant expression.
-    std::string space(int m) {
-        if (m == W) return "1";
-        if (goff.count(m)) return "(GTOP ? 0 : 1)";
-        return "1";
-    }
+    // State space (SP_GLOBAL 0 / SP_SHARED 1) of a stage, as a placeholder (see stage()).
+    std::string space(int m) { return "@P" + std::to_string(m) + "@"; }
 
     void child(int id, const std::string& src) {
         const Node& v = t.nodes[id];
@@ -443,6 +458,7 @@ struct CtaEmitter {
             if (helper && h == W && r.kind != Kind::Rate0) emit("if (gtid<T>() < 32) sync.helper_arrive();");
             emit("cG0R<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
             emit("sync();");
+            emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
             if (id == 0) emit("sync.root_g_done();");
             child(v.right, D);
             emit("cComb0R<T, " + N_ + ">(" + B + ");");
@@ -452,11 +468,13 @@ struct CtaEmitter {
         if (helper && h == W) emit("if (gtid<T>() < 32) sync.helper_arrive();");
         emit("cF<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
         emit("sync();");
+        emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
         child(v.left, D);
         if (r.kind == Kind::Rate0) return;
         if (helper && h == W) emit("if (gtid<T>() < 32) sync.helper_arrive();");
         emit("cG<P, T, " + N_ + ", " + CL + ", false, " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ", " + B + ");");
         emit("sync();");
+        emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
         if (id == 0) emit("sync.root_g_done();");
         child(v.right, D);
         emit("cComb<T, " + N_ + ">(" + B + ");");
@@ -669,11 +687,12 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     if (!cta_phase) {
         o << "    static constexpr int STAGE_ELEMS = 0;\n    static constexpr int STAGE_ELEMS_SMEM = 0;\n"
           << "    static constexpr int GSTAGE_ELEMS = 0;\n    static constexpr int WST = 0;\n"
+          << "    static constexpr int STAGE_BYTES_SMEM_H = 0;\n    static constexpr int GSTAGE_BYTES_H = 0;\n"
           << "    static constexpr bool GBETA = false;\n    static constexpr int HELPER = 0;\n"
           << "    template <class P, class SyncT>\n"
           << "    static PD_INLINE void helper(const float*, uint32_t*, const SyncT&) {}\n";
         emit_warp_sub(o, t, 0, "decode_root", &sh, true);  // reads the channel
-        o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
+        o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, bool H16, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t*, typename P::st_t*, typename P::v_t*,\n"
           << "                                 uint32_t* beta, const SyncT&) {\n"
           << "        if (gtid<T>() < 32) decode_root<P>(chan, beta);\n    }\n";
@@ -685,23 +704,31 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         ce.XW = sp.xw;
         ce.helper = sp.helper > 0;
         ce.latni = sp.latni;
-        int acc = 0, sacc = 0, gacc = 0;
+        int acc = 0, sacc = 0, gacc = 0, hs = 0, hg = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
+        ce.h16 = sp.h16;
         for (int m = sp.N / 2; m >= W; m /= 2) {
             ce.stage_off[m] = acc;
             acc += m;
+            const int hb = m * (m <= sp.h16 ? 2 : 1);  // H16 layout bytes (int8 profile)
             if (m >= gs) {
                 ce.goff[m] = gacc;
                 gacc += m;
+                ce.hoff[m] = hg;
+                hg += hb;
             } else {
                 ce.soff[m] = sacc;
                 sacc += m;
+                ce.hoff[m] = hs;
+                hs += hb;
             }
         }
         ce.cta(0, "chan");
         o << "    static constexpr int STAGE_ELEMS = " << acc << ";\n"
           << "    static constexpr int STAGE_ELEMS_SMEM = " << sacc << ";  // GTOP layout\n"
           << "    static constexpr int GSTAGE_ELEMS = " << gacc << ";\n"
+          << "    static constexpr int STAGE_BYTES_SMEM_H = " << hs << ";  // H16 layout (int8 throughput)\n"
+          << "    static constexpr int GSTAGE_BYTES_H = " << hg << ";\n"
           << "    static constexpr int WST = " << W << ";  // f32 stage feeding the register subtrees\n"
           << "    static constexpr bool GBETA = " << (sp.gbeta && gacc > 0 ? "true" : "false") << ";\n"
           << "    static constexpr int HELPER = " << (ce.helper ? sp.helper : 0) << ";  // helper warp on scheduler HELPER-1\n";
@@ -712,7 +739,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         if (ce.helper)
             for (auto& f : ce.lat_subs) o << "        sync.helper_wait();\n        " << f << "<P>(dsrc, dbeta);\n";
         o << "    }\n";
-        o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, class ChanT, class SyncT>\n"
+        o << "    template <class P, int T, bool GTOP, bool WF32, int CHS, bool H16, class ChanT, class SyncT>\n"
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
           << "                                 typename P::v_t* wst, uint32_t* beta, const SyncT& sync) {\n"
           << "        constexpr bool NI = T == 32 && N >= 8192;  // shared non-inlined stage ops\n"
@@ -768,20 +795,25 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         bool gtop;
         int minb;
         bool lat;
+        bool h16;
     };
     auto bytes = [&](const char* prof) { return sp.N * (std::string(prof) == "PF32" ? 4 : 1); };
     // Throughput variant: as many lockstep warps (frames) per CTA as the shared memory of one
     // SM holds, at most 16 (same formula as FrameLayout::PER_FRAME).
     auto a16 = [](int x) { return (x + 15) & ~15; };
-    int g_elems = 0;
+    int g_elems = 0, h_smem = 0, h_glob = 0;  // H16 layout bytes (as emit_struct computes them)
     if (cta_phase) {
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
-        for (int m = sp.N / 2; m >= W; m /= 2)
-            if (m >= gs) g_elems += m;
+        for (int m = sp.N / 2; m >= W; m /= 2) {
+            const int hb = m * (m <= sp.h16 ? 2 : 1);
+            if (m >= gs) g_elems += m, h_glob += hb;
+            else h_smem += hb;
+        }
     }
+    const bool h16 = cta_phase && sp.h16 > 0;
     auto fpc = [&](const char* prof, bool chan_smem) {
         const int s = std::string(prof) == "PF32" ? 4 : 1;
-        const int stages = a16(std::max(0, cta_phase ? sp.N - W - g_elems : 0) * s);
+        const int stages = (h16 && s == 1) ? a16(h_smem) : a16(std::max(0, cta_phase ? sp.N - W - g_elems : 0) * s);
         const int outw = a16((sp.K + 31) / 32 * 4);
         const bool gb = sp.gbeta && g_elems > 0;
         const int per = (chan_smem ? 2 * a16(sp.N * s) : 0) + stages + (gb ? 0 : a16(std::max(1, sp.N / 32) * 4)) +
@@ -791,15 +823,15 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     const bool cs_f = 2 * bytes("PF32") <= 16384, cs_i = 2 * bytes("PI8") <= 16384;
     const bool gt = g_elems > 0;
     std::vector<V> vars = {
-        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f), gt, 1, false},
-        {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i), gt, sp.cps, false},
-        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1, false, 1, true},
-        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1, false, 1, true},
+        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f), gt, 1, false, false},
+        {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i), gt, sp.cps, false, h16},
+        {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1, false, 1, true, false},
+        {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1, false, 1, true, false},
     };
     for (auto& v : vars) {
         const std::string targs = std::string("pd::") + v.prof + ", " + (v.lat ? CL : C) + ", " + std::to_string(v.T) + ", " +
                                   std::to_string(v.fpc) + ", " + (v.chan_smem ? "true" : "false") + ", " +
-                                  (v.gtop ? "true" : "false");
+                                  (v.gtop ? "true" : "false") + ", " + (v.h16 ? "true" : "false");
         const std::string kargs = targs + ", " + std::to_string(v.minb);
         o << "extern const void* const polar_kern_" << sp.name << "_" << v.tag << " = (const void*)&pd::k_frame<"
           << kargs << ">;\n"
@@ -823,7 +855,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         const std::string km = "pd::k_mailbox<pd::PI8, " + CL + ", " + std::to_string(t_lat) + ">";
         o << "extern const void* const polar_kern_" << sp.name << "_mbox_i8 = (const void*)&" << km << ";\n"
           << "extern const unsigned polar_smem_" << sp.name << "_mbox_i8 = pd::FrameLayout<pd::PI8, " << CL << ", "
-          << t_lat << ", 1, true, false>::SMEM;\n";
+          << t_lat << ", 1, true, false, false>::SMEM;\n";
         reg_decl << "extern const void* const polar_kern_" << sp.name << "_mbox_i8;\n"
                  << "extern const unsigned polar_smem_" << sp.name << "_mbox_i8;\n";
     }
@@ -844,7 +876,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     for (auto& v : vars)
         reg_entries << ", {&polar_kern_" << sp.name << "_" << v.tag << ", &polar_smem_" << sp.name << "_" << v.tag
                     << ", " << v.T << ", " << v.fpc << ", "
-                    << (v.gtop ? a16(g_elems * (std::string(v.prof) == "PF32" ? 4 : 1)) +
+                    << (v.gtop ? (v.h16 ? a16(h_glob) : a16(g_elems * (std::string(v.prof) == "PF32" ? 4 : 1))) +
                                      (sp.gbeta ? a16(std::max(1, sp.N / 32) * 4) : 0)
                                : 0)
                     << ", " << (v.lat && sp.helper && sp.N > WL ? 32 * sp.helper : 0) << "}";
@@ -911,6 +943,7 @@ int main(int argc, char** argv) {
             else if (opt.rfind("T=", 0) == 0) sp.T = std::atoi(opt.c_str() + 2);
             else if (opt.rfind("FPC=", 0) == 0) sp.fpc_max = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("GS=", 0) == 0) sp.gs = std::atoi(opt.c_str() + 3);
+            else if (opt.rfind("H16=", 0) == 0) sp.h16 = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("LL=", 0) == 0) sp.ll = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("CPS=", 0) == 0) sp.cps = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("WLAT=", 0) == 0) sp.wlat = std::atoi(opt.c_str() + 5);

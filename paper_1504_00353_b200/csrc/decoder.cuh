@@ -69,6 +69,62 @@ static __device__ unsigned long long* g_ptrace;
     do {          \
     } while (0)
 #endif
+// POLAR_DEBUG_DUMP builds (libpolar_dump.so, test infrastructure): every F / G / G_0R output
+// vector is appended, in the decoder's op order, to a per-frame float array (the alpha stages
+// the north star's f32 bar compares with the oracle, 1e-5 relative).  The frame's array and
+// its fill position live in shared memory per warp index: the warp of a throughput frame
+// group, 0 for the latency CTA (only its warp 0 runs the register subtrees).
+// floats per frame in the dump: every level of the tree holds at most N F/G outputs
+__host__ __device__ constexpr int dump_stride(int N) {
+    int l = 0;
+    while ((1 << l) < N) ++l;
+    return N * (l > 0 ? l : 1);
+}
+#ifdef POLAR_DEBUG_DUMP
+__shared__ float* s_dbase[32];
+__shared__ int s_dpos[32];
+PD_INLINE unsigned dump_slot() { return threadIdx.x >> 5; }
+// register outputs of a warp op: n/2 values, element i at (lane i mod 32, slot i / 32) when
+// n >= 64, replicated (lane l holds element l mod n/2) when n <= 32
+template <int n, class V>
+PD_INLINE void dump_reg(const V* c) {
+    const unsigned w = dump_slot();
+    float* const d = s_dbase[w] + s_dpos[w];
+    if constexpr (n >= 64) {
+#pragma unroll
+        for (int j = 0; j < n / 64; ++j) d[(threadIdx.x & 31u) + 32 * j] = (float)c[j];
+    } else {
+        if ((threadIdx.x & 31u) < (unsigned)(n / 2)) d[threadIdx.x & 31u] = (float)c[0];
+    }
+    __syncwarp();
+    if ((threadIdx.x & 31u) == 0) s_dpos[w] += n / 2;
+    __syncwarp();
+}
+PD_INLINE float dump_val(float x) { return x; }
+PD_INLINE float dump_val(int8_t x) { return (float)x; }
+PD_INLINE float dump_val(__half x) { return __half2float(x); }
+// a stage written by a CTA-scope op: h elements at p (group of T threads)
+template <int T, class S>
+PD_INLINE void dump_stage(const S* p, int h) {
+    const unsigned w = T == 32 ? dump_slot() : 0u;
+    const int tid = T == 32 ? (int)(threadIdx.x & 31u) : (int)threadIdx.x;
+    float* const d = s_dbase[w] + s_dpos[w];
+    for (int i = tid; i < h; i += T) d[i] = dump_val(p[i]);
+    if constexpr (T == 32) __syncwarp(); else asm volatile("bar.sync 1, %0;" ::"n"(T) : "memory");
+    if (tid == 0) s_dpos[w] += h;
+    if constexpr (T == 32) __syncwarp(); else asm volatile("bar.sync 1, %0;" ::"n"(T) : "memory");
+}
+#define PD_DUMPR(n, c) dump_reg<n>(c)
+#define PD_DUMPS(p, h) dump_stage<T>(p, h)
+#else
+#define PD_DUMPR(n, c) \
+    do {               \
+    } while (0)
+#define PD_DUMPS(p, h) \
+    do {               \
+    } while (0)
+#endif
+
 // Index of the thread in its frame group of T threads (T = 32: the lane).
 template <int T>
 PD_INLINE int gtid() { return T == 32 ? (int)(threadIdx.x & 31u) : (int)threadIdx.x; }
@@ -119,6 +175,7 @@ struct PI8 {
     static PD_INLINE v_t ld(int8_t x) { return __int_as_float(0x4B400000 + max((int)x, -127)) - 12582912.0f; }
     static PD_INLINE int8_t st(v_t x) { return (int8_t)__float2int_rn(x); }
     static PD_INLINE v_t ld(float x) { return x; }  // the f32 subtree-input stage
+    static PD_INLINE v_t ld(__half x) { return __half2float(x); }  // f16 stages (exact integers)
     static PD_INLINE v_t f(v_t a, v_t b) { return PF32::f(a, b); }
     // saturating adder (max(-127) P:848): clamp(x) = copysign(min(|x|, 127), x)
     static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) { return fminxs(PF32::g(a, b, beta), 127.0f); }
@@ -229,14 +286,15 @@ struct Chunk<PF32, CE> {
     static_assert(CE == 4, "");
     float v[4];
     uint32_t w[4];
-    template <int SP, int H = L2_NORMAL>
-    PD_INLINE void load_raw(const void* p) { vld<SP, 16, H>(p, w); }
+    template <int SP, int H, class S>
+    PD_INLINE void load_raw(const S* p) { vld<SP, 16, H>(p, w); }
+    template <class S>
     PD_INLINE void unpack_raw(bool = false) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) v[k] = __uint_as_float(w[k]);
     }
-    template <int SP, bool F32OUT, int H = L2_NORMAL>
-    PD_INLINE void store(void* p) const {
+    template <int SP, int H, class D>
+    PD_INLINE void store(D* p) const {
         const uint32_t w[4] = {__float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]), __float_as_uint(v[3])};
         vst<SP, 16, H>(p, w);
     }
@@ -262,13 +320,38 @@ struct Chunk<PI8, CE> {
         }
     }
     uint32_t w[CE / 4];
-    template <int SP, int H = L2_NORMAL>
-    PD_INLINE void load_raw(const void* p) { vld<SP, CE, H>(p, w); }
-    PD_INLINE void unpack_raw(bool clamp) { unpack(w, clamp); }
-    // F32OUT: the f32 stage feeding the register subtrees (latency variant), else int8
-    template <int SP, bool F32OUT, int H = L2_NORMAL>
-    PD_INLINE void store(void* p) const {
-        if constexpr (F32OUT) {
+    // Source S: int8 (channel or an int8 stage: CE bytes, unpacked after the load) or __half
+    // (an f16 stage: the CE values load straight into h[], no conversion).
+    template <int SP, int H, class S>
+    PD_INLINE void load_raw(const S* p) {
+        if constexpr (sizeof(S) == 1) {
+            vld<SP, CE, H>(p, w);
+        } else {
+            static_assert(sizeof(S) == 2, "");
+            if constexpr (CE == 16) {
+                vld<SP, 16, H>(p, h);
+                vld<SP, 16, H>((const S*)p + 8, h + 4);
+            } else {
+                vld<SP, 2 * CE, H>(p, h);
+            }
+        }
+    }
+    template <class S>
+    PD_INLINE void unpack_raw(bool clamp) {
+        if constexpr (sizeof(S) == 1) unpack(w, clamp);
+    }
+    // D: float (the f32 stage feeding the register subtrees, latency variant), __half (an f16
+    // stage: h[] stored as is) or int8
+    template <int SP, int H, class D>
+    PD_INLINE void store(D* p) const {
+        if constexpr (sizeof(D) == 2) {
+            if constexpr (CE == 16) {
+                vst<SP, 16, H>(p, h);
+                vst<SP, 16, H>(p + 8, h + 4);
+            } else {
+                vst<SP, 2 * CE, H>(p, h);
+            }
+        } else if constexpr (sizeof(D) == 4) {
 #pragma unroll
             for (int q = 0; q < CE / 4; ++q) {
                 const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&h[2 * q]));
@@ -399,6 +482,7 @@ PD_INLINE void wF(const Src& s, typename P::v_t* c) {
         s.pair(n / 2, x, y);
         c[0] = P::f(x, y);
     }
+    PD_DUMPR(n, c);
 }
 
 // G<n>: child[i] = g(alpha[i], alpha[i + n/2], beta_l[i]); beta_l from bw slots
@@ -429,6 +513,7 @@ PD_INLINE void wG(const Src& s, typename P::v_t* c, uint64_t bw, uint32_t ml) {
         c[0] = P::g0(xa, ya);
 #endif
     }
+    PD_DUMPR(n, c);
 }
 
 // G_0R<n>: G with beta_l = 0 (left child Rate-0); b + a is symmetric.
@@ -442,6 +527,7 @@ PD_INLINE void wG0R(const Src& s, typename P::v_t* c) {
         s.pair(n / 2, x, y);
         c[0] = P::g0(x, y);
     }
+    PD_DUMPR(n, c);
 }
 
 // Rate-1 / Info<n> (eq:info P:444-449): beta = hard decisions.
@@ -671,10 +757,8 @@ __host__ __device__ constexpr int stage_unroll() {
     constexpr int umax = T == 32 ? 4 : 1;  // the latency CTA (shared-memory stages, 128-register cap) needs none
     return H / step >= umax ? umax : H / step >= 2 ? 2 : 1;
 }
-template <class P, int T, int n, bool CLAMP, int SS, int DS, bool F32OUT>
+template <class P, int T, int n, bool CLAMP, int SS, int DS, class S, class D>
 PD_INLINE void cF_body(const void* src, void* dst) {
-    using S = typename P::st_t;
-    using D = typename std::conditional<F32OUT, float, S>::type;
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>(), STEP = CE * T, U = stage_unroll<P, H, T>();
     constexpr int LH = CLAMP ? L2_FIRST : L2_LAST;
 #pragma unroll 1
@@ -689,17 +773,15 @@ PD_INLINE void cF_body(const void* src, void* dst) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (i0 + u * STEP < H) {
-                a[u].unpack_raw(CLAMP);
-                b[u].unpack_raw(CLAMP);
+                a[u].template unpack_raw<S>(CLAMP);
+                b[u].template unpack_raw<S>(CLAMP);
                 chunk_f(a[u], b[u]);
-                a[u].template store<DS, F32OUT, L2_LAST>((D*)dst + i0 + u * STEP);
+                a[u].template store<DS, L2_LAST>((D*)dst + i0 + u * STEP);
             }
     }
 }
-template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, bool F32OUT>
+template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, class S, class D>
 PD_INLINE void cG_body(const void* src, void* dst, const uint32_t* beta) {
-    using S = typename P::st_t;
-    using D = typename std::conditional<F32OUT, float, S>::type;
     constexpr int H = n / 2, CE = chunk_elems<P, H, T>(), STEP = CE * T, U = stage_unroll<P, H, T>();
     constexpr int LH = CLAMP ? L2_FIRST : L2_LAST;
 #pragma unroll 1
@@ -717,35 +799,33 @@ PD_INLINE void cG_body(const void* src, void* dst, const uint32_t* beta) {
 #pragma unroll
         for (int u = 0; u < U; ++u)
             if (i0 + u * STEP < H) {
-                a[u].unpack_raw(CLAMP);
-                b[u].unpack_raw(CLAMP);
+                a[u].template unpack_raw<S>(CLAMP);
+                b[u].template unpack_raw<S>(CLAMP);
                 if constexpr (ZERO_LEFT) chunk_g0(a[u], b[u]);
                 else chunk_g(a[u], b[u], bits[u]);
-                a[u].template store<DS, F32OUT, L2_LAST>((D*)dst + i0 + u * STEP);
+                a[u].template store<DS, L2_LAST>((D*)dst + i0 + u * STEP);
             }
     }
 }
-template <class P, int T, int n, bool CLAMP, int SS, int DS, bool F32OUT>
+template <class P, int T, int n, bool CLAMP, int SS, int DS, class S, class D>
 __device__ __noinline__ void cF_impl(const void* src, void* dst) {
-    cF_body<P, T, n, CLAMP, SS, DS, F32OUT>(src, dst);
+    cF_body<P, T, n, CLAMP, SS, DS, S, D>(src, dst);
 }
-template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, bool F32OUT>
+template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, class S, class D>
 __device__ __noinline__ void cG_impl(const void* src, void* dst, const uint32_t* beta) {
-    cG_body<P, T, n, CLAMP, ZERO_LEFT, SS, DS, F32OUT>(src, dst, beta);
+    cG_body<P, T, n, CLAMP, ZERO_LEFT, SS, DS, S, D>(src, dst, beta);
 }
 // NI: call the shared non-inlined instance (throughput variant of large codes); otherwise
 // inline (the call costs latency on the batch-1 critical path).
 template <class P, int T, int n, bool CLAMP, int SS, int DS, bool NI, class TS, class TD>
 PD_INLINE void cF(const TS* src, TD* dst) {
-    constexpr bool F32OUT = sizeof(TD) == 4 && sizeof(typename P::st_t) == 1;
-    if constexpr (NI) cF_impl<P, T, n, CLAMP, SS, DS, F32OUT>(src, dst);
-    else cF_body<P, T, n, CLAMP, SS, DS, F32OUT>(src, dst);
+    if constexpr (NI) cF_impl<P, T, n, CLAMP, SS, DS, TS, TD>(src, dst);
+    else cF_body<P, T, n, CLAMP, SS, DS, TS, TD>(src, dst);
 }
 template <class P, int T, int n, bool CLAMP, bool ZERO_LEFT, int SS, int DS, bool NI, class TS, class TD>
 PD_INLINE void cG(const TS* src, TD* dst, const uint32_t* beta) {
-    constexpr bool F32OUT = sizeof(TD) == 4 && sizeof(typename P::st_t) == 1;
-    if constexpr (NI) cG_impl<P, T, n, CLAMP, ZERO_LEFT, SS, DS, F32OUT>(src, dst, beta);
-    else cG_body<P, T, n, CLAMP, ZERO_LEFT, SS, DS, F32OUT>(src, dst, beta);
+    if constexpr (NI) cG_impl<P, T, n, CLAMP, ZERO_LEFT, SS, DS, TS, TD>(src, dst, beta);
+    else cG_body<P, T, n, CLAMP, ZERO_LEFT, SS, DS, TS, TD>(src, dst, beta);
 }
 template <class P, int T, int n, bool CLAMP, int SS, int DS, bool NI, class TS, class TD>
 PD_INLINE void cG0R(const TS* src, TD* dst) {

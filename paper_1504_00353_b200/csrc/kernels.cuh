@@ -62,7 +62,7 @@ struct OpSync {
     }
 };
 
-template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP>
+template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP, bool H16>
 struct FrameLayout {
     using in_t = typename P::in_t;
     using st_t = typename P::st_t;
@@ -74,7 +74,9 @@ struct FrameLayout {
     // WF32 (latency variant): the stage of size W, read element by element by the register
     // subtrees, is kept as f32 in its own array
     static constexpr bool WF32 = T > 32;
-    static constexpr int WST_OFF = align16((GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t));
+    // H16: the int8 throughput variant's stages of size <= the code's H16 option are f16
+    static constexpr int WST_OFF =
+        align16(H16 ? C::STAGE_BYTES_SMEM_H : (GTOP ? C::STAGE_ELEMS_SMEM : C::STAGE_ELEMS) * (int)sizeof(st_t));
     static constexpr int STAGES = WST_OFF + (WF32 ? align16(C::WST * (int)sizeof(typename P::v_t)) : 0);
     // helper warp (latency variant, Code::HELPER): dummy subtree input and decision bits
     static constexpr bool HELP = WF32 && C::HELPER > 0;
@@ -84,7 +86,7 @@ struct FrameLayout {
     static constexpr bool GB = GTOP && C::GBETA;
     static constexpr int BETA_BYTES = align16((C::N >= 32 ? C::N / 32 : 1) * 4);
     static constexpr int BETA = GB ? 0 : BETA_BYTES;
-    static constexpr int GSTAGE_BYTES = align16(C::GSTAGE_ELEMS * (int)sizeof(st_t));
+    static constexpr int GSTAGE_BYTES = align16(H16 ? C::GSTAGE_BYTES_H : C::GSTAGE_ELEMS * (int)sizeof(st_t));
     static constexpr int GSLOT = GSTAGE_BYTES + (GB ? BETA_BYTES : 0);  // global bytes per slot
     // output staging words: the stage area is free after the decode when it is large enough
     static constexpr int OUTW = align16((C::K + 31) / 32 * 4);
@@ -96,12 +98,16 @@ struct FrameLayout {
 // FPC frame groups of T threads per CTA (FPC > 1 only with T = 32).
 // GTOP: the largest stages (N/2 and N/4 by default) live in global scratch (L2-resident), one slot per frame
 // group of the persistent grid, so that more frames fit in shared memory per SM.
-template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP, int MINB = 1>
+template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP, bool H16, int MINB = 1>
 __global__ void __launch_bounds__(T * FPC + (T > 32 ? 32 * C::HELPER : 0), MINB)
     k_frame(const void* __restrict__ llr_, long long n_frames, uint32_t* __restrict__ out,
-            const uint32_t* __restrict__ gtab, void* __restrict__ gscratch) {
+            const uint32_t* __restrict__ gtab, void* __restrict__ gscratch
+#ifdef POLAR_DEBUG_DUMP
+            , float* __restrict__ dump  // [n_frames][dump_stride(N)] alpha stages (decoder.cuh)
+#endif
+    ) {
     static_assert(FPC == 1 || T == 32, "");
-    using L = FrameLayout<P, C, T, FPC, CHAN_SMEM, GTOP>;
+    using L = FrameLayout<P, C, T, FPC, CHAN_SMEM, GTOP, H16>;
     using in_t = typename P::in_t;
     using st_t = typename P::st_t;
     constexpr int N = C::N;
@@ -200,7 +206,15 @@ __global__ void __launch_bounds__(T * FPC + (T > 32 ? 32 * C::HELPER : 0), MINB)
             for (int k = tid; k < N / 32; k += T) beta[k] = 0;
             sync();
         }
-        C::template decode<P, T, GTOP, L::WF32, CHAN_SMEM ? SP_SHARED : SP_GLOBAL>(chan, stages, gst, wst, beta, sync);
+#ifdef POLAR_DEBUG_DUMP
+        if (leader) {
+            const unsigned w = T == 32 ? (threadIdx.x >> 5) : 0u;
+            s_dbase[w] = dump + f * (long long)dump_stride(N);
+            s_dpos[w] = 0;
+        }
+        if constexpr (T == 32) __syncwarp(); else group_sync<T>();
+#endif
+        C::template decode<P, T, GTOP, L::WF32, CHAN_SMEM ? SP_SHARED : SP_GLOBAL, H16>(chan, stages, gst, wst, beta, sync);
         sync();
         gather_info<N, C::K, T>(beta, gtab, stg, out + f * NWK);
         sync();
@@ -254,7 +268,7 @@ __global__ void __launch_bounds__(T, 1)
     static_assert(T > 32 && C::N % 16 == 0 && C::N >= 64, "");
     // the frame goes straight from host-mapped memory into the shared-memory channel buffer
     // (as the TMA copy of k_frame's latency variant would put it); dbuf is unused
-    using L = FrameLayout<P, C, T, 1, true, false>;
+    using L = FrameLayout<P, C, T, 1, true, false, false>;
     constexpr int N = C::N;
     extern __shared__ __align__(128) unsigned char smem_all[];
     __shared__ unsigned int s_req;
@@ -297,7 +311,7 @@ __global__ void __launch_bounds__(T, 1)
         if constexpr (C::STAGE_ELEMS > 0)
             for (int k = threadIdx.x; k < N / 32; k += T) beta[k] = 0;
         __syncthreads();
-        C::template decode<P, T, false, L::WF32, SP_SHARED>((const int8_t*)chan, stages, (st_t*)nullptr, wst, beta, sync);
+        C::template decode<P, T, false, L::WF32, SP_SHARED, false>((const int8_t*)chan, stages, (st_t*)nullptr, wst, beta, sync);
         sync();
         gather_info<N, C::K, T>(beta, gtab, stg, hout);
         __threadfence_system();

@@ -80,6 +80,7 @@ struct polar_code {
     cudaStream_t sc_last[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     bool sc_used[5] = {false, false, false, false, false};
     unsigned long long* d_trace = nullptr;  // POLAR_TRACE builds: per-op clock64 of the latency variant
+    float* d_dump = nullptr;                // POLAR_DEBUG_DUMP builds: alpha stages of up to kDumpFrames frames
     uint32_t* d_info_mask = nullptr;  // N/32 words (>= 1), bit set = information position
     // host-buffer path (lazily allocated, guarded by mu)
     std::mutex mu;
@@ -108,6 +109,13 @@ static inline uint32_t words_of(uint32_t bits) { return (bits + 31) / 32; }
 #define POLAR_DYN 1
 #endif
 constexpr size_t kScratchHdr = 256;
+// POLAR_DEBUG_DUMP: frames per dumped decode and floats per frame (decoder.cuh dump_stride)
+constexpr int64_t kDumpFrames = 8;
+static uint64_t dump_stride(uint32_t N) {
+    uint32_t l = 0;
+    while ((1u << l) < N) ++l;
+    return (uint64_t)N * (l > 0 ? l : 1);
+}
 
 extern "C" const char* polar_status_string(polar_status s) {
     switch (s) {
@@ -185,6 +193,9 @@ static polar_status init_device(polar_code* h) {
     CUDA_TRY(cudaMemcpy(h->d_gtab, gt.data(), gt.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMalloc(&h->d_info_mask, im.size() * sizeof(uint32_t)));
     CUDA_TRY(cudaMemcpy(h->d_info_mask, im.data(), im.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+#ifdef POLAR_DEBUG_DUMP
+    CUDA_TRY(cudaMalloc(&h->d_dump, kDumpFrames * dump_stride(h->N) * sizeof(float)));
+#endif
 #ifdef POLAR_TRACE
     CUDA_TRY(cudaMalloc(&h->d_trace, 65536 * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemset(h->d_trace, 0, 65536 * sizeof(unsigned long long)));
@@ -237,6 +248,7 @@ extern "C" void polar_code_destroy(polar_code* h) {
     // every resource that exists is released, also after a partial init_device (cudaFree(nullptr)
     // is a no-op; the pointers start null)
     if (h->d_trace) cudaFree(h->d_trace);
+    if (h->d_dump) cudaFree(h->d_dump);
     if (h->d_prog) cudaFree(h->d_prog);
     if (h->d_pos) cudaFree(h->d_pos);
     if (h->d_info_mask) cudaFree(h->d_info_mask);
@@ -304,6 +316,29 @@ extern "C" polar_status polar_trace_fetch(const polar_code* h, uint64_t* host, u
 #else
     (void)n;
     return fail(POLAR_ERR_UNSUPPORTED_CODE, "not a POLAR_TRACE build");
+#endif
+}
+
+extern "C" polar_status polar_debug_dump_stride(const polar_code* h, uint64_t* stride) {
+    if (!h || !stride) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
+#ifdef POLAR_DEBUG_DUMP
+    *stride = dump_stride(h->N);
+    return POLAR_OK;
+#else
+    return fail(POLAR_ERR_UNSUPPORTED_CODE, "not a POLAR_DEBUG_DUMP build");
+#endif
+}
+
+extern "C" polar_status polar_debug_dump_fetch(const polar_code* h, float* host, uint64_t n) {
+    if (!h || !host) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
+#ifdef POLAR_DEBUG_DUMP
+    if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device");
+    if (n > (uint64_t)kDumpFrames * dump_stride(h->N)) return fail(POLAR_ERR_INVALID_ARGUMENT, "n exceeds the dump");
+    CUDA_TRY(cudaMemcpy(host, h->d_dump, n * sizeof(float), cudaMemcpyDeviceToHost));
+    return POLAR_OK;
+#else
+    (void)n;
+    return fail(POLAR_ERR_UNSUPPORTED_CODE, "not a POLAR_DEBUG_DUMP build");
 #endif
 }
 
@@ -408,7 +443,14 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
 #ifdef POLAR_TRACE
     if (lat) gs = h->d_trace;
 #endif
+#ifdef POLAR_DEBUG_DUMP
+    if (n > kDumpFrames) return fail(POLAR_ERR_INVALID_ARGUMENT, "POLAR_DEBUG_DUMP build: at most %d frames", (int)kDumpFrames);
+    CUDA_TRY(cudaMemsetAsync(h->d_dump, 0xff, kDumpFrames * dump_stride(h->N) * sizeof(float), s));  // NaN
+    float* dump = h->d_dump;
+    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs, (void*)&dump};
+#else
     void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs};
+#endif
     return launch_with_scratch(h, vi, kern, dim3(grid), dim3(v.threads * v.frames + v.extra), args, smem, s);
 }
 

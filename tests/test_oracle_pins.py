@@ -133,6 +133,11 @@ def test_worked_8_5_frame():
     assert g0r == [float(v) for v in g["g0r4"]]
     g8 = [oracle.g_f32(a[0, i], a[0, i + 4], 1) for i in range(4)]
     assert g8 == [float(v) for v in g["g8"]]
+    # the oracle's alpha dump (the reference side of the GPU alpha-stage parity test) records
+    # exactly the hand trace's F<8>, G_0R<4>, G<8> outputs in Listing-1 order
+    want = [float(v) for k in ("f8", "g0r4", "g8") for v in g[k]]
+    assert oracle.fastssc_alpha_dump(frozen, a[0]).tolist() == want
+    assert oracle.fastssc_alpha_dump(frozen, np.rint(4 * a[0]).astype(np.int8)).tolist() == [4 * v for v in want]
 
 
 # ------------------------------------------------------------------ node decoders are ML (brute force)
