@@ -393,22 +393,46 @@ def main():
         extra["latency_batch1_2048_1723"] = latency_batch1(CODE2)
     N, K = main_r["N"], main_r["K"]
     B = main_r["B"]
-    # Roofline: the decode kernel is ALU/issue bound.  Algorithmic work
-    # = elementary LLR operations per frame (f, g, leaf elements) x frames; peak = one lane-op
-    # per lane per clock on every SM at the max SM clock.
-    elem = {29492: 104500 + 106042 + 31226}[K]
-    sm_mhz = 1965.0
-    peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # T lane-ops/s
-    achieved = elem * B / (main_r["launch_ms"] * 1e-3) / 1e12
-    hbm_bytes = B * (N + 4 * code_words(K))
-    # DRAM bytes per frame measured by ncu (--set full) on the same kernel, scaled to this
-    # launch (profiles/traffic.json, written from the capture named there).
-    traffic = None
+    # Roofline.  Headline: HBM -- algorithmic bytes per frame (the channel
+    # LLRs read once + the packed information bits written once) x frames / the decode launch's
+    # average CUDA-event duration, against MEASURED_PEAKS.json's copy bandwidth.  The kernel is
+    # bound inside the SM, so the same line carries its fractions of the measured SM ceilings
+    # (profiles/peaks_sm.json, tools/sm_peaks.cu): ALU pipe, issue slots and shared memory, each
+    # = the ncu-counted work per frame of this kernel (profiles/roofline_inputs.json, from the
+    # capture named there) x the frames/s measured here / the ceiling at the SM clock sampled
+    # during the timed region.
+    frames_per_s = B / (main_r["launch_ms"] * 1e-3)
+    hbm_bytes_frame = N + 4 * code_words(K)
+    peaks = {}
     try:
-        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        traffic = tj["c32768_29492_i8_tp"]["dram_bytes_per_frame"] * B
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback 6.65 TB/s"
+    hbm_ach = hbm_bytes_frame * frames_per_s / 1e9
+    sm_clk = (main_r["clocks"].get("sm_mhz") or 1965.0) * 1e6
+    ri, psm = {}, {}
+    try:
+        ri = json.load(open(os.path.join(ROOT, "profiles", "roofline_inputs.json")))["c32768_29492_i8_tp"]
+        psm = json.load(open(os.path.join(ROOT, "profiles", "peaks_sm.json")))["pipes"]
     except (OSError, KeyError, ValueError):
         pass
+    ceilings = {}
+    if ri and psm:
+        nsm = 148
+        alu_peak = psm["LOP3"]["warp_inst_per_clk_per_sm"] * nsm * sm_clk
+        ceilings["alu_pipe"] = {"achieved": ri["alu_warp_inst_per_frame"] * frames_per_s, "peak": alu_peak,
+                                "unit": "warp inst/s", "frac": ri["alu_warp_inst_per_frame"] * frames_per_s / alu_peak}
+        iss_peak = 4 * nsm * sm_clk
+        ceilings["issue"] = {"achieved": ri["warp_inst_per_frame"] * frames_per_s, "peak": iss_peak,
+                             "unit": "warp inst/s", "frac": ri["warp_inst_per_frame"] * frames_per_s / iss_peak}
+        smem_peak = psm["LDS128"]["per_clk_per_sm"] * nsm * sm_clk / 128.0  # 128-byte wavefronts/s
+        ceilings["smem"] = {"achieved": ri["smem_wavefronts_per_frame"] * frames_per_s, "peak": smem_peak,
+                            "unit": "wavefronts/s", "frac": ri["smem_wavefronts_per_frame"] * frames_per_s / smem_peak}
+        ceilings["source"] = (f"per-frame work: ncu capture {ri['capture']} (profiles/roofline_inputs.json); "
+                              "ceilings: profiles/peaks_sm.json (tools/sm_peaks.cu) at the sampled SM clock")
+    traffic = ri.get("dram_bytes_per_frame", 0) * B if ri else None
     line = {
         "metric": "info_gbps", "value": main_r["gbps"], "unit": "Gbps", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": main_r["ms_per_step"], "higher_is_better": True,
@@ -421,11 +445,11 @@ def main():
                    "l2_flush": "inputs larger than L2 (512 MiB int8 LLRs per GPU)", "parallelism": f"dp{ws}"},
         "e2e": main_r["e2e"],
         "gpu_launches": args.steps,
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s (lane-ops)",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per frame x frames per launch)",
-                     "hbm_achieved_gbs": hbm_bytes / (main_r["launch_ms"] * 1e-3) / 1e9,
-                     "hbm_frac_of_measured": hbm_bytes / (main_r["launch_ms"] * 1e-3) / 1e9 / 6554.6},
+        "roofline": {"bound": "hbm", "achieved": hbm_ach, "peak": hbm_peak, "unit": "GB/s", "frac": hbm_ach / hbm_peak,
+                     "traffic": traffic, "peak_source": hbm_src,
+                     "algorithmic_bytes_per_frame": hbm_bytes_frame,
+                     "traffic_source": "ncu dram__bytes_read+write per frame (profiles/roofline_inputs.json) x frames per launch",
+                     "sm_ceilings": ceilings},
         "clocks": main_r["clocks"],
         "fer": main_r["fer"], "ber": main_r["ber"],
         "extra": extra,

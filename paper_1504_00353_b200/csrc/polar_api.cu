@@ -189,6 +189,29 @@ static polar_status init_device(polar_code* h) {
         gt.push_back(acc);
         acc += (uint32_t)__builtin_popcount(w);
     }
+    // Piece table of the unrolled kernels' gather (decoder.cuh gather_info): output word q of
+    // x_hat[A] is the OR of its pieces -- maximal runs of information positions that stay in one
+    // codeword word and one output word -- each {codeword word, source shift, destination
+    // shift, mask}.  Layout after the two tables above: offsets[NWK + 1] (padded to 4 words),
+    // then the pieces as uint4.
+    {
+        const uint32_t nwk = words_of(h->K);
+        std::vector<uint32_t> off(nwk + 1, 0), pcs;
+        for (uint32_t j = 0; j < (uint32_t)pos.size();) {
+            const uint32_t q = j / 32, src = pos[j], k = src / 32;
+            uint32_t len = 1;
+            while (j + len < (uint32_t)pos.size() && (j + len) / 32 == q && pos[j + len] == src + len && (src + len) / 32 == k)
+                ++len;
+            pcs.insert(pcs.end(), {k, src % 32, j % 32, len >= 32 ? 0xffffffffu : ((1u << len) - 1u)});
+            off[q + 1] = (uint32_t)(pcs.size() / 4);
+            j += len;
+        }
+        for (uint32_t q = 1; q <= nwk; ++q) off[q] = std::max(off[q], off[q - 1]);
+        while (off.size() % 4) off.push_back(0);
+        while (gt.size() % 4) gt.push_back(0);
+        gt.insert(gt.end(), off.begin(), off.end());
+        gt.insert(gt.end(), pcs.begin(), pcs.end());
+    }
     CUDA_TRY(cudaMalloc(&h->d_gtab, gt.size() * sizeof(uint32_t)));
     CUDA_TRY(cudaMemcpy(h->d_gtab, gt.data(), gt.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMalloc(&h->d_info_mask, im.size() * sizeof(uint32_t)));
