@@ -84,9 +84,25 @@ polar_status polar_code_query(const polar_code* h, uint32_t* N, uint32_t* K, uin
  * terminating NUL into buf (may be NULL); *needed (may be NULL) receives the full size. */
 polar_status polar_code_schedule(const polar_code* h, char* buf, uint32_t cap, uint32_t* needed);
 
-/* *specialised = 1 if the handle uses a decoder unrolled for its code at build time, 0 if it
- * uses the generic program-interpreted decoder. */
+/* *specialised = 1 if the handle uses a decoder unrolled for its code at build time, 2 if
+ * polar_code_create specialised one at run time (below), 0 if it uses the generic
+ * program-interpreted decoder (then polar_last_error() says why the run-time specialisation
+ * did not happen). */
 polar_status polar_code_is_specialised(const polar_code* h, int* specialised);
+
+/* Run-time specialisation (the paper generates an unrolled decoder per code):
+ * polar_code_create gives a frozen set without a build-time decoder its own, generated by the
+ * library's code generator and compiled with NVRTC for sm_100a (the four throughput/latency x
+ * float/int8 kernels; no frame-interleaved or mailbox kernel).  Compiled cubins are cached on
+ * disk under a hash of the generated source ($POLAR_JIT_CACHE, default ~/.cache/polar_jit) and
+ * shared by handles of the same code in a process.  POLAR_JIT=0 disables it (generic decoder);
+ * so does an unrolled length above POLAR_JIT_MAX_OPS Fast-SSC ops (default 4096: the GA codes
+ * of this repo have 300-3,600; a random frozen set of N = 32768 has ~60,000, where -- as the
+ * paper says of long codes, P:1277 -- the instruction-based decoder is the practical one).
+ * POLAR_JIT_FORCE=1 specialises at run time even codes that have a build-time decoder.
+ * polar_jit_compile runs the generation and compilation only (no device needed), for checks:
+ * POLAR_OK and the cache tag in log, or POLAR_ERR_UNSUPPORTED_CODE and NVRTC's log. */
+polar_status polar_jit_compile(uint32_t N, uint32_t K, const uint8_t* frozen_mask, char* log, uint32_t cap);
 
 /* Kernel variant used by the decode calls: 0 = automatic (default: the latency variant,
  * one CTA per frame, when n_frames <= number of SMs (x4 for N >= 16384); for int8 codes with
@@ -97,6 +113,17 @@ polar_status polar_code_is_specialised(const polar_code* h, int* specialised);
  * Returns POLAR_ERR_INVALID_ARGUMENT for any other value.  Not thread-safe with concurrent
  * decode calls on the same handle. */
 polar_status polar_code_set_variant(polar_code* h, int variant);
+
+/* Information bits the decode calls return (default POLAR_OUTPUT_SYSTEMATIC):
+ *   POLAR_OUTPUT_SYSTEMATIC     x_hat[A], the systematic code's information bits (reading C4);
+ *   POLAR_OUTPUT_NONSYSTEMATIC  u_hat[A] with u_hat = x_hat G_N (G_N its own inverse):
+ *                               the information bits of the non-systematic code x = u G_N.
+ * Same decoder either way; the kernels apply the polar transform to the decoded codeword
+ * before the gather.  The frame-interleaved variant (4) is systematic only (its decode calls
+ * then return POLAR_ERR_UNSUPPORTED_CODE); a mailbox opened afterwards uses the mode.  Not
+ * thread-safe with concurrent decode calls on the same handle. */
+enum { POLAR_OUTPUT_SYSTEMATIC = 0, POLAR_OUTPUT_NONSYSTEMATIC = 1 };
+polar_status polar_code_set_output(polar_code* h, int mode);
 
 /* Copy the handle's frozen mask (N bytes, 1 = frozen) into host buffer mask_out. */
 polar_status polar_code_mask(const polar_code* h, uint8_t* mask_out);

@@ -62,6 +62,10 @@ def lib():
         L.or_fastssc_dump_f32.restype = C.c_long
         L.or_fastssc_dump_i8.argtypes = [C.c_int, _u8p, _i8p, _u8p, _i32p, C.c_long]
         L.or_fastssc_dump_i8.restype = C.c_long
+        L.or_nodeset_decode_f32.argtypes = [C.c_int, _u8p, C.c_void_p, C.c_long, C.c_void_p, C.c_int]
+        L.or_nodeset_decode_i8.argtypes = [C.c_int, _u8p, C.c_void_p, C.c_long, C.c_void_p, C.c_int]
+        L.or_nodeset_trace.argtypes = [C.c_int, _u8p, C.c_int, C.c_char_p, C.c_int]
+        L.or_nodeset_trace.restype = C.c_int
         L.or_ml_decode_f32.argtypes = [C.c_int, _u8p, _f32p, C.c_long, _u8p]
         L.or_rep_f32.argtypes = [C.c_int, _f32p, _u8p]
         L.or_spc_f32.argtypes = [C.c_int, _f32p, _u8p]
@@ -197,6 +201,40 @@ def fastssc_decode(frozen: np.ndarray, llr: np.ndarray, threads: int = 1) -> np.
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(run, range(threads)))
     return xhat
+
+
+NODE_SETS = {"fastssc": 0, "nospc": 1, "ssc": 2, "sc": 3}
+
+
+def nodeset_decode(frozen: np.ndarray, llr: np.ndarray, node_set: str, threads: int = 1) -> np.ndarray:
+    """O2's traversal restricted to a node set ('fastssc', 'nospc', 'ssc', 'sc'; the paper's
+    algorithm ablation): xhat uint8[n, N]."""
+    frozen = np.ascontiguousarray(frozen, np.uint8)
+    N = frozen.shape[0]
+    is_i8 = np.asarray(llr).dtype == np.int8
+    a = _frames(llr, N, np.int8 if is_i8 else np.float32)
+    n = a.shape[0]
+    xhat = np.empty((n, N), np.uint8)
+    fn = lib().or_nodeset_decode_i8 if is_i8 else lib().or_nodeset_decode_f32
+    bounds = np.linspace(0, n, max(1, threads) + 1).astype(np.int64)
+
+    def run(t):
+        lo, hi = int(bounds[t]), int(bounds[t + 1])
+        if hi > lo:
+            fn(N, frozen, a[lo:hi].ctypes.data, hi - lo, xhat[lo:hi].ctypes.data, NODE_SETS[node_set])
+
+    with ThreadPoolExecutor(max(1, threads)) as ex:
+        list(ex.map(run, range(max(1, threads))))
+    return xhat
+
+
+def nodeset_trace(frozen: np.ndarray, node_set: str) -> list[str]:
+    frozen = np.ascontiguousarray(frozen, np.uint8)
+    N = frozen.shape[0]
+    cap = 64 * N + 64
+    buf = C.create_string_buffer(cap)
+    lib().or_nodeset_trace(N, frozen, NODE_SETS[node_set], buf, cap)
+    return [t for t in buf.value.decode().split(";") if t]
 
 
 def fastssc_trace(frozen: np.ndarray) -> list[str]:

@@ -297,12 +297,26 @@ typedef struct {
     char* buf;
     int cap;
     int len;
+    /* node set (0 Fast-SSC, 1 no SPC, 2 SSC, 3 plain SC): the paper's algorithm ablation
+     * (tab:impl:tp:algo-unroll; the GPU decoder without SPC nodes P:1134-1136) */
+    int set;
     /* optional alpha dump: every F / G / G_0R output vector appended in op order (the
      * intermediate LLRs the north star's float bar compares, 1e-5 relative); records only */
     float* af;
     int* ai;
     long apos, acap;
 } or_trace;
+
+/* or_classify restricted to the trace's node set: SC splits every node of size > 1, SSC
+ * keeps only Rate-0 / Rate-1, "no SPC" keeps Rate-0 / Rate-1 / repetition. */
+static int classify_set(int n, const uint8_t* frozen, const or_trace* tr) {
+    const int set = tr ? tr->set : 0;
+    if (set == 3 && n > 1) return OR_SPLIT;
+    const int k = or_classify(n, frozen);
+    if (set == 2 && (k == OR_REP || k == OR_SPC)) return OR_SPLIT;
+    if (set == 1 && k == OR_SPC) return OR_SPLIT;
+    return k;
+}
 
 static void dump_f32(or_trace* tr, const float* v, int h) {
     if (!tr || !tr->af) return;
@@ -336,7 +350,7 @@ static void trace_op(or_trace* tr, const char* name, int n) {
 
 static void fssc_f32(int n, const uint8_t* frozen, const float* alpha, uint8_t* beta,
                      float* scratch, or_trace* tr) {
-    int kind = or_classify(n, frozen);
+    int kind = classify_set(n, frozen, tr);
     if (kind == OR_RATE0) { for (int i = 0; i < n; ++i) beta[i] = 0; return; }
     if (kind == OR_RATE1) {
         trace_op(tr, "Info", n);
@@ -347,7 +361,7 @@ static void fssc_f32(int n, const uint8_t* frozen, const float* alpha, uint8_t* 
     if (kind == OR_SPC) { trace_op(tr, "SPC", n); or_spc_f32(n, alpha, beta); return; }
     int h = n / 2;
     float* child = scratch;
-    int left = or_classify(h, frozen), right = or_classify(h, frozen + h);
+    int left = classify_set(h, frozen, tr), right = classify_set(h, frozen + h, tr);
     if (left == OR_RATE0) {
         trace_op(tr, "G_0R", n);
         for (int i = 0; i < h; ++i) { beta[i] = 0; child[i] = or_g_f32(alpha[i], alpha[i + h], 0); }
@@ -376,7 +390,7 @@ static void fssc_f32(int n, const uint8_t* frozen, const float* alpha, uint8_t* 
 
 static void fssc_i8(int n, const uint8_t* frozen, const int* alpha, uint8_t* beta,
                     int* scratch, or_trace* tr) {
-    int kind = or_classify(n, frozen);
+    int kind = classify_set(n, frozen, tr);
     if (kind == OR_RATE0) { for (int i = 0; i < n; ++i) beta[i] = 0; return; }
     if (kind == OR_RATE1) {
         trace_op(tr, "Info", n);
@@ -387,7 +401,7 @@ static void fssc_i8(int n, const uint8_t* frozen, const int* alpha, uint8_t* bet
     if (kind == OR_SPC) { trace_op(tr, "SPC", n); or_spc_i8(n, alpha, beta); return; }
     int h = n / 2;
     int* child = scratch;
-    int left = or_classify(h, frozen), right = or_classify(h, frozen + h);
+    int left = classify_set(h, frozen, tr), right = classify_set(h, frozen + h, tr);
     if (left == OR_RATE0) {
         trace_op(tr, "G_0R", n);
         for (int i = 0; i < h; ++i) { beta[i] = 0; child[i] = or_g_i8(alpha[i], alpha[i + h], 0); }
@@ -434,12 +448,46 @@ void or_fastssc_decode_i8(int N, const uint8_t* frozen, const int8_t* llr, long 
     free(in);
 }
 
+/* O2 restricted to a node set (set: 0 Fast-SSC = or_fastssc_decode_*, 1 no SPC, 2 SSC,
+ * 3 plain SC through the same traversal): the references of the GPU ablation builds. */
+void or_nodeset_decode_f32(int N, const uint8_t* frozen, const float* llr, long n_frames, uint8_t* xhat, int set) {
+    float* scratch = (float*)malloc(sizeof(float) * (size_t)N);
+    or_trace tr = {NULL, 0, 0, set, NULL, NULL, 0, 0};
+    for (long fr = 0; fr < n_frames; ++fr) fssc_f32(N, frozen, llr + fr * N, xhat + fr * N, scratch, &tr);
+    free(scratch);
+}
+
+void or_nodeset_decode_i8(int N, const uint8_t* frozen, const int8_t* llr, long n_frames, uint8_t* xhat, int set) {
+    int* in = (int*)malloc(sizeof(int) * (size_t)N);
+    int* scratch = (int*)malloc(sizeof(int) * (size_t)N);
+    or_trace tr = {NULL, 0, 0, set, NULL, NULL, 0, 0};
+    for (long fr = 0; fr < n_frames; ++fr) {
+        for (int i = 0; i < N; ++i) in[i] = ingest_i8(llr[fr * N + i]);
+        fssc_i8(N, frozen, in, xhat + fr * N, scratch, &tr);
+    }
+    free(scratch);
+    free(in);
+}
+
+int or_nodeset_trace(int N, const uint8_t* frozen, int set, char* buf, int cap) {
+    float* llr = (float*)calloc((size_t)N, sizeof(float));
+    float* scratch = (float*)malloc(sizeof(float) * (size_t)N);
+    uint8_t* xhat = (uint8_t*)malloc((size_t)N);
+    or_trace tr = {buf, cap, 0, set, NULL, NULL, 0, 0};
+    if (cap > 0) buf[0] = 0;
+    fssc_f32(N, frozen, llr, xhat, scratch, &tr);
+    free(xhat);
+    free(scratch);
+    free(llr);
+    return tr.len;
+}
+
 /* Listing-1-style trace of the op sequence O2 executes on one f32 frame ("F<8>;G_0R<4>;..."). */
 int or_fastssc_trace(int N, const uint8_t* frozen, char* buf, int cap) {
     float* llr = (float*)calloc((size_t)N, sizeof(float));
     float* scratch = (float*)malloc(sizeof(float) * (size_t)N);
     uint8_t* xhat = (uint8_t*)malloc((size_t)N);
-    or_trace tr = {buf, cap, 0, NULL, NULL, 0, 0};
+    or_trace tr = {buf, cap, 0, 0, NULL, NULL, 0, 0};
     if (cap > 0) buf[0] = 0;
     fssc_f32(N, frozen, llr, xhat, scratch, &tr);
     free(xhat);
@@ -452,7 +500,7 @@ int or_fastssc_trace(int N, const uint8_t* frozen, char* buf, int cap) {
  * returns the number of values written (at most cap).  The decode itself is unchanged. */
 long or_fastssc_dump_f32(int N, const uint8_t* frozen, const float* llr, uint8_t* xhat, float* out, long cap) {
     float* scratch = (float*)malloc(sizeof(float) * (size_t)N);
-    or_trace tr = {NULL, 0, 0, out, NULL, 0, cap};
+    or_trace tr = {NULL, 0, 0, 0, out, NULL, 0, cap};
     fssc_f32(N, frozen, llr, xhat, scratch, &tr);
     free(scratch);
     return tr.apos;
@@ -462,7 +510,7 @@ long or_fastssc_dump_i8(int N, const uint8_t* frozen, const int8_t* llr, uint8_t
     int* in = (int*)malloc(sizeof(int) * (size_t)N);
     int* scratch = (int*)malloc(sizeof(int) * (size_t)N);
     for (int i = 0; i < N; ++i) in[i] = ingest_i8(llr[i]);
-    or_trace tr = {NULL, 0, 0, NULL, out, 0, cap};
+    or_trace tr = {NULL, 0, 0, 0, NULL, out, 0, cap};
     fssc_i8(N, frozen, in, xhat, scratch, &tr);
     free(scratch);
     free(in);

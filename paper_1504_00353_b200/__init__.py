@@ -26,12 +26,12 @@ POLAR_ERR_OUT_OF_MEMORY = 4
 EXPORTS = [
     "polar_status_string", "polar_last_error", "polar_code_create", "polar_code_destroy",
     "polar_code_query", "polar_code_schedule", "polar_code_mask", "polar_code_set_variant",
-    "polar_code_is_specialised", "polar_decode_f32",
+    "polar_code_is_specialised", "polar_code_set_output", "polar_decode_f32",
     "polar_decode_i8", "polar_decode_f32_host", "polar_decode_i8_host", "polar_mailbox_open",
     "polar_mailbox_decode_i8", "polar_mailbox_close", "polar_construct_ga",
     "polar_encode_systematic", "polar_gen_bpsk_awgn", "polar_count_errors",
     "polar_registry_size", "polar_registry_entry", "polar_trace_fetch", "polar_debug_dump_stride",
-    "polar_debug_dump_fetch",
+    "polar_debug_dump_fetch", "polar_jit_compile",
 ]
 
 
@@ -71,6 +71,7 @@ def _load(path: str) -> C.CDLL:
         "polar_code_schedule": (C.c_int, [vp, C.c_char_p, C.c_uint32, u32p]),
         "polar_code_mask": (C.c_int, [vp, vp]),
         "polar_code_set_variant": (C.c_int, [vp, C.c_int]),
+        "polar_code_set_output": (C.c_int, [vp, C.c_int]),
         "polar_code_is_specialised": (C.c_int, [vp, C.POINTER(C.c_int)]),
         "polar_decode_f32": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
         "polar_decode_i8": (C.c_int, [vp, vp, C.c_int64, vp, vp]),
@@ -88,9 +89,12 @@ def _load(path: str) -> C.CDLL:
         "polar_trace_fetch": (C.c_int, [vp, vp, C.c_uint32]),
         "polar_debug_dump_stride": (C.c_int, [vp, C.POINTER(C.c_uint64)]),
         "polar_debug_dump_fetch": (C.c_int, [vp, vp, C.c_uint64]),
+        "polar_jit_compile": (C.c_int, [C.c_uint32, C.c_uint32, vp, C.c_char_p, C.c_uint32]),
         "polar_registry_entry": (C.c_int, [C.c_uint32, u32p, u32p, vp]),
     }
     for name, (res, args) in sig.items():
+        if not hasattr(L, name):  # an older experiment build (tools/variant_build.sh); tests check the product's
+            continue
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
@@ -128,6 +132,15 @@ def construct_ga(N: int, K: int, design_ebn0_db: float) -> np.ndarray:
     return m
 
 
+def jit_compile(N: int, K: int, frozen_mask: np.ndarray) -> str:
+    """Generate and NVRTC-compile the unrolled decoder of a frozen set (no device needed);
+    returns the cache tag, raises PolarError with NVRTC's log on failure."""
+    m = np.ascontiguousarray(np.asarray(frozen_mask, np.uint8))
+    buf = C.create_string_buffer(4096)
+    _check(lib().polar_jit_compile(N, K, m.ctypes.data, buf, 4096))
+    return buf.value.decode()
+
+
 def registry() -> list[tuple[int, int, np.ndarray]]:
     """(N, K, frozen mask) of every code specialised into this build."""
     L = lib()
@@ -159,6 +172,7 @@ class PolarCode:
         sp = C.c_int()
         self._chk(self._L.polar_code_is_specialised(h, C.byref(sp)))
         self.specialised = bool(sp.value)
+        self.run_time_specialised = sp.value == 2
 
     def _chk(self, status: int) -> None:
         _check(status, self._L)
@@ -190,6 +204,10 @@ class PolarCode:
     def set_variant(self, variant: str) -> None:
         """'auto' | 'throughput' | 'latency' | 'generic' (all decode identically)."""
         self._chk(self._L.polar_code_set_variant(self._h, {"auto": 0, "throughput": 1, "latency": 2, "generic": 3, "xframe": 4}[variant]))
+
+    def set_output(self, mode: str) -> None:
+        """'systematic' (x_hat[A], default) | 'nonsystematic' (u_hat[A], u_hat = x_hat G_N)."""
+        self._chk(self._L.polar_code_set_output(self._h, {"systematic": 0, "nonsystematic": 1}[mode]))
 
     def mask(self) -> np.ndarray:
         m = np.zeros(self.N, np.uint8)

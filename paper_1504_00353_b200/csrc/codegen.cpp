@@ -21,6 +21,7 @@
 #include <string>
 #include <vector>
 
+#include "jit.hpp"
 #include "tree.hpp"
 
 namespace polar {
@@ -54,6 +55,7 @@ struct Spec {
     bool gbeta = false;   // throughput variant: decision bits in the global slot scratch too (GBETA=1)
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
     int h16 = 0;          // int8 throughput variant: stages of size <= h16 stored as f16 (H16=; 0: none)
+    NodeSet nodes = NodeSet::FastSSC;  // NODES=fastssc|nospc|ssc|sc: the algorithm ablation (tree.hpp)
     int xsm = 48 * 1024;  // frame-interleaved variant: shared-memory budget per warp (XSM=; 24K/48K/72K
                           // measured 162/262/207 Gbps at (2048,1723), profiles/r1_history.md)
     int xwpc = 1;         // frame-interleaved variant: warps per CTA (XWPC=)
@@ -663,9 +665,10 @@ std::string mask_string(const std::vector<uint8_t>& m) {
     return s;
 }
 
+// jit != nullptr: run-time specialisation -- the source and the variants go to *jit, no files.
 void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& reg_decl,
-               std::ostringstream& reg_entries) {
-    Tree t = build_tree(sp.N, sp.mask.data());
+               std::ostringstream& reg_entries, JitCode* jit = nullptr) {
+    Tree t = build_tree(sp.N, sp.mask.data(), sp.nodes);
     std::vector<std::string> ops = schedule(t);
     const int W = std::min(sp.N, sp.W);
     const bool cta_phase = sp.N > W;
@@ -828,11 +831,24 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1, false, 1, true, false},
         {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1, false, 1, true, false},
     };
+    // the host-side registry symbols exist only in the build-time (nvcc) compilation
+    o << "#ifndef __CUDACC_RTC__\n";
+    auto gscratch_of = [&](const V& v) {
+        return v.gtop ? (v.h16 ? a16(h_glob) : a16(g_elems * (std::string(v.prof) == "PF32" ? 4 : 1))) +
+                            (sp.gbeta ? a16(std::max(1, sp.N / 32) * 4) : 0)
+                      : 0;
+    };
+    int vi = 0;
     for (auto& v : vars) {
         const std::string targs = std::string("pd::") + v.prof + ", " + (v.lat ? CL : C) + ", " + std::to_string(v.T) + ", " +
                                   std::to_string(v.fpc) + ", " + (v.chan_smem ? "true" : "false") + ", " +
                                   (v.gtop ? "true" : "false") + ", " + (v.h16 ? "true" : "false");
         const std::string kargs = targs + ", " + std::to_string(v.minb);
+        if (jit) {
+            jit->vars[vi++] = JitVariant{"&pd::k_frame<" + kargs + ">", "pd::FrameLayout<" + targs + ">::SMEM", (uint32_t)v.T,
+                                         (uint32_t)v.fpc, (uint32_t)gscratch_of(v),
+                                         (uint32_t)(v.lat && sp.helper && sp.N > WL ? 32 * sp.helper : 0)};
+        }
         o << "extern const void* const polar_kern_" << sp.name << "_" << v.tag << " = (const void*)&pd::k_frame<"
           << kargs << ">;\n"
           << "extern const unsigned polar_smem_" << sp.name << "_" << v.tag << " = pd::FrameLayout<" << targs
@@ -859,6 +875,24 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         reg_decl << "extern const void* const polar_kern_" << sp.name << "_mbox_i8;\n"
                  << "extern const unsigned polar_smem_" << sp.name << "_mbox_i8;\n";
     }
+    o << "#else\n";
+    // NVRTC: the shared-memory sizes, read back by polar_api.cu (cudaLibraryGetGlobal)
+    if (jit) {
+        o << "extern \"C\" __device__ unsigned polar_jit_smem[4] = {";
+        for (int i = 0; i < 4; ++i) o << (i ? ", " : "") << jit->vars[i].smem;
+        o << "};\n";
+    }
+    o << "#endif\n";
+    std::string sched;
+    for (auto& s : ops) sched += s + ";";
+    if (jit) {
+        jit->source = o.str();
+        jit->n_ops = (uint32_t)ops.size();
+        jit->warp_root = (uint32_t)W;
+        jit->schedule = sched;
+        g_marks = nullptr;
+        return;
+    }
     std::ofstream(outdir + "/code_" + sp.name + ".cu") << o.str();
     {
         std::ofstream tl(outdir + "/trace_" + sp.name + ".txt");
@@ -866,8 +900,6 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     }
     g_marks = nullptr;
 
-    std::string sched;
-    for (auto& s : ops) sched += s + ";";
     reg_decl << "static const uint8_t mask_" << sp.name << "[" << sp.N << "] = {";
     for (int i = 0; i < sp.N; ++i) reg_decl << (i ? "," : "") << int(sp.mask[i]);
     reg_decl << "};\n";
@@ -875,10 +907,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
                 << code_hash(sp.N, sp.K, sp.mask.data()) << "ull, " << ops.size() << ", " << W;
     for (auto& v : vars)
         reg_entries << ", {&polar_kern_" << sp.name << "_" << v.tag << ", &polar_smem_" << sp.name << "_" << v.tag
-                    << ", " << v.T << ", " << v.fpc << ", "
-                    << (v.gtop ? (v.h16 ? a16(h_glob) : a16(g_elems * (std::string(v.prof) == "PF32" ? 4 : 1))) +
-                                     (sp.gbeta ? a16(std::max(1, sp.N / 32) * 4) : 0)
-                               : 0)
+                    << ", " << v.T << ", " << v.fpc << ", " << gscratch_of(v)
                     << ", " << (v.lat && sp.helper && sp.N > WL ? 32 * sp.helper : 0) << "}";
     reg_entries << ", {&polar_kern_" << sp.name << "_xf_i8, &polar_smem_" << sp.name << "_xf_i8, 32, " << sp.xwpc
                 << ", 0, 0}, &polar_gslot_" << sp.name << "_xf_i8";
@@ -892,6 +921,11 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
 
 }  // namespace
 
+namespace {
+void parse_options(Spec& sp, std::istream& ls);
+}
+
+#ifndef POLAR_CODEGEN_LIB
 int main(int argc, char** argv) {
     if (argc != 3) {
         std::cerr << "usage: polar_codegen <spec file> <output dir>\n";
@@ -937,6 +971,22 @@ int main(int argc, char** argv) {
             std::cerr << "codegen: unknown construction " << how << "\n";
             return 2;
         }
+        parse_options(sp, ls);
+        specs.push_back(sp);
+    }
+    std::ostringstream decl, entries;
+    for (auto& sp : specs) emit_code(sp, argv[2], decl, entries);
+    std::ostringstream reg;
+    reg << "// Generated by codegen.cpp. Do not edit.\n#include \"registry.hpp\"\n\n" << decl.str()
+        << "\nnamespace polar {\nconst RegistryEntry kRegistry[] = {\n" << entries.str() << "};\n"
+        << "const uint32_t kRegistrySize = " << specs.size() << ";\n}  // namespace polar\n";
+    std::ofstream(std::string(argv[2]) + "/registry.cpp") << reg.str();
+    return 0;
+}
+#endif  // POLAR_CODEGEN_LIB
+
+namespace {
+void parse_options(Spec& sp, std::istream& ls) {
         std::string opt;
         while (ls >> opt) {
             if (opt.rfind("W=", 0) == 0) sp.W = std::atoi(opt.c_str() + 2);
@@ -944,6 +994,10 @@ int main(int argc, char** argv) {
             else if (opt.rfind("FPC=", 0) == 0) sp.fpc_max = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("GS=", 0) == 0) sp.gs = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("H16=", 0) == 0) sp.h16 = std::atoi(opt.c_str() + 4);
+            else if (opt.rfind("NODES=", 0) == 0) {
+                const std::string v = opt.substr(6);
+                sp.nodes = v == "sc" ? NodeSet::SC : v == "ssc" ? NodeSet::SSC : v == "nospc" ? NodeSet::NoSPC : NodeSet::FastSSC;
+            }
             else if (opt.rfind("LL=", 0) == 0) sp.ll = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("CPS=", 0) == 0) sp.cps = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("WLAT=", 0) == 0) sp.wlat = std::atoi(opt.c_str() + 5);
@@ -962,14 +1016,29 @@ int main(int argc, char** argv) {
                     if (tok != "none") sp.dedup.insert(std::atoi(tok.c_str()));
             }
         }
-        specs.push_back(sp);
-    }
-    std::ostringstream decl, entries;
-    for (auto& sp : specs) emit_code(sp, argv[2], decl, entries);
-    std::ostringstream reg;
-    reg << "// Generated by codegen.cpp. Do not edit.\n#include \"registry.hpp\"\n\n" << decl.str()
-        << "\nnamespace polar {\nconst RegistryEntry kRegistry[] = {\n" << entries.str() << "};\n"
-        << "const uint32_t kRegistrySize = " << specs.size() << ";\n}  // namespace polar\n";
-    std::ofstream(std::string(argv[2]) + "/registry.cpp") << reg.str();
-    return 0;
 }
+}  // namespace
+
+namespace polar {
+// Default options by code length: those of the registered codes in codes.txt.
+bool codegen_jit(int N, int K, const uint8_t* frozen, JitCode* out, std::string* err) {
+    if (N < 2 || (N & (N - 1)) || N > 32768 || K < 1 || K > N) {
+        if (err) *err = "bad (N, K)";
+        return false;
+    }
+    Spec sp;
+    sp.name = "jit";
+    sp.N = N;
+    sp.K = K;
+    sp.mask.assign(frozen, frozen + N);
+    std::istringstream opts(N >= 16384 ? "W=512 FPC=6 CPS=3 DEDUP=32"
+                            : N == 8192 ? "W=512 T=512 GS=2048 DEDUP=16,32,64"
+                            : N == 4096 ? "W=1024 T=256"
+                            : N == 2048 ? "W=2048 WLAT=1024 FPC=8 CPS=2"
+                                        : "");
+    parse_options(sp, opts);
+    std::ostringstream decl, entries;
+    emit_code(sp, "", decl, entries, out);
+    return true;
+}
+}  // namespace polar

@@ -22,10 +22,21 @@
 //  * PI8 : int8 storage, int32 registers; g saturates to [-127, 127] (reading C8).
 #pragma once
 
+#ifdef __CUDACC_RTC__
+// NVRTC (run-time specialisation of an unregistered code, polar_api.cu jit_code): no host
+// standard headers; the fixed-width types the kernels use.
+typedef signed char int8_t;
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#include <cuda_fp16.h>
+#else
 #include <cstdint>
-#include <type_traits>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#endif
 
 namespace pd {
 
@@ -981,6 +992,29 @@ PD_INLINE uint32_t pext32(uint32_t x, uint32_t m) {
         m &= ~(lm << s);
     }
     return r;
+}
+
+// Non-systematic output (reading C4): u_hat = x_hat G_N, computed in place on the N-bit array
+// (x G_N: x[j] ^= x[j | d] for every bit d of the index, G_N[i][j] = [j subset of i])
+// by the T threads of the frame group; the information bits are then u_hat[A].
+template <int N, int T>
+PD_INLINE void beta_transform(uint32_t* beta) {
+    constexpr int NW = N >= 32 ? N / 32 : 1;
+    constexpr uint32_t in_word[5] = {0x55555555u, 0x33333333u, 0x0F0F0F0Fu, 0x00FF00FFu, 0x0000FFFFu};
+#pragma unroll
+    for (int b = 0; b < 5; ++b) {
+        if ((1 << b) >= N) break;
+        for (int k = gtid<T>(); k < NW; k += T) {
+            const uint32_t x = beta[k];
+            beta[k] = x ^ ((x >> (1 << b)) & in_word[b]);
+        }
+        group_sync<T>();
+    }
+    for (int D = 1; D < NW; D <<= 1) {
+        for (int k = gtid<T>(); k < NW; k += T)
+            if (!(k & D)) beta[k] ^= beta[k | D];
+        group_sync<T>();
+    }
 }
 
 // Piece-table gather (tab after the {imask, prefix} words: offsets[NWK + 1] padded to 4 words,

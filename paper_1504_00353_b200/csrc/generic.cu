@@ -32,7 +32,8 @@ PD_INLINE void put_bits(uint32_t* beta, int off, int n, uint32_t bits) {
 template <class P>
 __global__ void __launch_bounds__(32) k_generic(const void* __restrict__ llr_, long long n_frames,
                                                 uint32_t* __restrict__ out, const uint32_t* __restrict__ gtab,
-                                                const uint32_t* __restrict__ prog, int n_ops, int N, int K) {
+                                                const uint32_t* __restrict__ prog, int n_ops, int N, int K,
+                                                unsigned flags) {
     using S = typename P::st_t;
     using V = typename P::v_t;
     extern __shared__ __align__(16) unsigned char gsmem[];
@@ -152,7 +153,19 @@ __global__ void __launch_bounds__(32) k_generic(const void* __restrict__ llr_, l
             }
             __syncwarp();
         }
-        // systematic information bits x_hat[A] (as gather_info, runtime sizes)
+        if (flags & 1u) {  // non-systematic: u_hat = x_hat G_N in place (as beta_transform)
+            const uint32_t in_word[5] = {0x55555555u, 0x33333333u, 0x0F0F0F0Fu, 0x00FF00FFu, 0x0000FFFFu};
+            for (int b = 0; b < 5 && (1 << b) < N; ++b) {
+                for (int k = l; k < NB; k += 32) beta[k] ^= (beta[k] >> (1 << b)) & in_word[b];
+                __syncwarp();
+            }
+            for (int D = 1; D < NB; D <<= 1) {
+                for (int k = l; k < NB; k += 32)
+                    if (!(k & D)) beta[k] ^= beta[k | D];
+                __syncwarp();
+            }
+        }
+        // information bits x_hat[A] (or u_hat[A]) (as gather_info, runtime sizes)
         for (int q = l; q < NWK; q += 32) stg[q] = 0;
         __syncwarp();
         for (int k = l; k < NB; k += 32) {

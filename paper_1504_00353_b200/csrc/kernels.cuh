@@ -101,7 +101,8 @@ struct FrameLayout {
 template <class P, class C, int T, int FPC, bool CHAN_SMEM, bool GTOP, bool H16, int MINB = 1>
 __global__ void __launch_bounds__(T * FPC + (T > 32 ? 32 * C::HELPER : 0), MINB)
     k_frame(const void* __restrict__ llr_, long long n_frames, uint32_t* __restrict__ out,
-            const uint32_t* __restrict__ gtab, void* __restrict__ gscratch
+            const uint32_t* __restrict__ gtab, void* __restrict__ gscratch,
+            unsigned flags  // bit 0: non-systematic output u_hat[A] (polar_code_set_output)
 #ifdef POLAR_DEBUG_DUMP
             , float* __restrict__ dump  // [n_frames][dump_stride(N)] alpha stages (decoder.cuh)
 #endif
@@ -216,6 +217,10 @@ __global__ void __launch_bounds__(T * FPC + (T > 32 ? 32 * C::HELPER : 0), MINB)
 #endif
         C::template decode<P, T, GTOP, L::WF32, CHAN_SMEM ? SP_SHARED : SP_GLOBAL, H16>(chan, stages, gst, wst, beta, sync);
         sync();
+        if (flags & 1u) {  // uniform per launch
+            if constexpr (T == 32) beta_transform<N, 32>(beta);
+            else beta_transform<N, T>(beta);
+        }
         gather_info<N, C::K, T>(beta, gtab, stg, out + f * NWK);
         sync();
         if constexpr (TMA && !DBL) {
@@ -264,7 +269,7 @@ PD_INLINE unsigned long long globaltimer_ns() {
 template <class P, class C, int T>
 __global__ void __launch_bounds__(T, 1)
     k_mailbox(const int8_t* __restrict__ hframe, uint32_t* __restrict__ hout, MailboxCtl* ctl, int8_t* __restrict__ dbuf,
-              const uint32_t* __restrict__ gtab, unsigned long long idle_ns) {
+              const uint32_t* __restrict__ gtab, unsigned long long idle_ns, unsigned flags) {
     static_assert(T > 32 && C::N % 16 == 0 && C::N >= 64, "");
     // the frame goes straight from host-mapped memory into the shared-memory channel buffer
     // (as the TMA copy of k_frame's latency variant would put it); dbuf is unused
@@ -313,6 +318,7 @@ __global__ void __launch_bounds__(T, 1)
         __syncthreads();
         C::template decode<P, T, false, L::WF32, SP_SHARED, false>((const int8_t*)chan, stages, (st_t*)nullptr, wst, beta, sync);
         sync();
+        if (flags & 1u) beta_transform<N, T>(beta);
         gather_info<N, C::K, T>(beta, gtab, stg, hout);
         __threadfence_system();
         __syncthreads();

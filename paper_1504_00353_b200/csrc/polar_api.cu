@@ -16,7 +16,17 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <unistd.h>
+#include <sys/stat.h>
+
+#include <fstream>
+#include <map>
+#include <memory>
+#include <sstream>
+
 #include "../../include/polar.h"
+#include "jit.hpp"
 #include "registry.hpp"
 #include "tree.hpp"
 
@@ -51,12 +61,211 @@ static polar_status fail(polar_status s, const char* fmt, ...) {
                         "%s: %s", #expr, cudaGetErrorString(e_));                         \
     } while (0)
 
+// ------------------------------------------------------------- run-time specialisation
+// An unregistered frozen set gets its unrolled decoder at create time, as the paper generates
+// one per code: codegen.cpp emits the source it would have written at build time,
+// NVRTC compiles the four k_frame variants for sm_100a, and the cubin is cached on disk under a
+// hash of the source (POLAR_JIT_CACHE, default ~/.cache/polar_jit) and in the process.  NVRTC is
+// opened at run time; without it, with POLAR_JIT=0 or on a compile error the code keeps the
+// generic program-interpreted decoder (same results, lower throughput).
+
+namespace {
+
+struct Nvrtc {
+    typedef int (*CreateFn)(void**, const char*, const char*, int, const char* const*, const char* const*);
+    typedef int (*CompileFn)(void*, int, const char* const*);
+    typedef int (*SizeFn)(void*, size_t*);
+    typedef int (*GetFn)(void*, char*);
+    typedef int (*NameFn)(void*, const char*);
+    typedef int (*LoweredFn)(void*, const char*, const char**);
+    typedef int (*DestroyFn)(void**);
+    void* so = nullptr;
+    CreateFn create = nullptr;
+    CompileFn compile = nullptr;
+    SizeFn log_size = nullptr, cubin_size = nullptr;
+    GetFn log = nullptr, cubin = nullptr;
+    NameFn add_name = nullptr;
+    LoweredFn lowered = nullptr;
+    DestroyFn destroy = nullptr;
+    bool ok() const { return create && compile && log_size && cubin_size && log && cubin && add_name && lowered && destroy; }
+};
+
+const Nvrtc& nvrtc() {
+    static Nvrtc n = [] {
+        Nvrtc r;
+        const char* names[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"};
+        for (const char* nm : names)
+            if ((r.so = dlopen(nm, RTLD_NOW | RTLD_LOCAL))) break;
+        if (!r.so) return r;
+        r.create = (Nvrtc::CreateFn)dlsym(r.so, "nvrtcCreateProgram");
+        r.compile = (Nvrtc::CompileFn)dlsym(r.so, "nvrtcCompileProgram");
+        r.log_size = (Nvrtc::SizeFn)dlsym(r.so, "nvrtcGetProgramLogSize");
+        r.cubin_size = (Nvrtc::SizeFn)dlsym(r.so, "nvrtcGetCUBINSize");
+        r.log = (Nvrtc::GetFn)dlsym(r.so, "nvrtcGetProgramLog");
+        r.cubin = (Nvrtc::GetFn)dlsym(r.so, "nvrtcGetCUBIN");
+        r.add_name = (Nvrtc::NameFn)dlsym(r.so, "nvrtcAddNameExpression");
+        r.lowered = (Nvrtc::LoweredFn)dlsym(r.so, "nvrtcGetLoweredName");
+        r.destroy = (Nvrtc::DestroyFn)dlsym(r.so, "nvrtcDestroyProgram");
+        return r;
+    }();
+    return n;
+}
+
+uint64_t fnv1a(const std::string& s, uint64_t h = 1469598103934665603ull) {
+    for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+    return h;
+}
+
+struct JitModule {
+    cudaLibrary_t lib = nullptr;
+    const void* kern[4] = {nullptr, nullptr, nullptr, nullptr};
+    unsigned smem[4] = {0, 0, 0, 0};
+    const void* none = nullptr;
+    unsigned zero = 0;
+    std::vector<uint8_t> mask;
+    std::string schedule;
+    RegistryEntry entry{};
+    ~JitModule() {
+        if (lib) cudaLibraryUnload(lib);
+    }
+};
+
+std::mutex g_jit_mu;
+std::map<std::pair<uint64_t, std::vector<uint8_t>>, std::weak_ptr<JitModule>> g_jit_cache;
+
+std::string jit_cache_dir() {
+    if (const char* d = std::getenv("POLAR_JIT_CACHE")) return d;
+    const char* home = std::getenv("HOME");
+    return std::string(home ? home : "/tmp") + "/.cache/polar_jit";
+}
+
+// Compile (or load from the disk cache) the unrolled decoder of an unregistered code.
+std::shared_ptr<JitModule> jit_build(uint32_t N, uint32_t K, const std::vector<uint8_t>& mask, std::string* why,
+                                     bool load = true) {
+    std::lock_guard<std::mutex> lock(g_jit_mu);
+    const auto key = std::make_pair(code_hash((int)N, (int)K, mask.data()), mask);
+    if (auto m = g_jit_cache[key].lock()) return m;
+    JitCode jc;
+    if (!codegen_jit((int)N, (int)K, mask.data(), &jc, why)) return nullptr;
+    std::string cuda_inc = "-I/usr/local/cuda/include";
+    if (const char* ch = std::getenv("CUDA_HOME")) cuda_inc = std::string("-I") + ch + "/include";
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", cuda_inc.c_str()};
+    uint64_t h = fnv1a(jc.source);
+    for (int i = 0; i < kJitHeaderCount; ++i) h = fnv1a(kJitHeaderText[i], h);
+    for (const char* o : opts) h = fnv1a(o, h);
+    char tag[64];
+    snprintf(tag, sizeof tag, "polar_%u_%u_%016llx", N, K, (unsigned long long)h);
+    const std::string dir = jit_cache_dir(), base = dir + "/" + tag;
+    std::string cubin;
+    std::vector<std::string> lowered(4);
+    if (std::getenv("POLAR_JIT_NO_CACHE")) {
+    } else {  // disk cache: <base>.cubin + <base>.names (the four lowered kernel names)
+        std::ifstream fc(base + ".cubin", std::ios::binary), fn(base + ".names");
+        if (fc && fn) {
+            cubin.assign(std::istreambuf_iterator<char>(fc), std::istreambuf_iterator<char>());
+            for (auto& l : lowered) std::getline(fn, l);
+            if (lowered[3].empty()) cubin.clear();
+        }
+    }
+    if (cubin.empty()) {
+        const Nvrtc& nv = nvrtc();
+        if (!nv.ok()) {
+            if (why) *why = "NVRTC (libnvrtc.so.12) not found";
+            return nullptr;
+        }
+        void* prog = nullptr;
+        if (nv.create(&prog, jc.source.c_str(), "polar_jit.cu", kJitHeaderCount, kJitHeaderText, kJitHeaderNames) != 0) {
+            if (why) *why = "nvrtcCreateProgram failed";
+            return nullptr;
+        }
+        for (auto& v : jc.vars) nv.add_name(prog, v.kernel.c_str());
+        const int rc = nv.compile(prog, 4, opts);
+        if (rc != 0) {
+            size_t n = 0;
+            nv.log_size(prog, &n);
+            std::string log(n, '\0');
+            nv.log(prog, &log[0]);
+            if (why) *why = "NVRTC compile failed: " + log.substr(0, 2000);
+            nv.destroy(&prog);
+            return nullptr;
+        }
+        for (int i = 0; i < 4; ++i) {
+            const char* ln = nullptr;
+            nv.lowered(prog, jc.vars[i].kernel.c_str(), &ln);
+            lowered[i] = ln ? ln : "";
+        }
+        size_t n = 0;
+        nv.cubin_size(prog, &n);
+        cubin.assign(n, '\0');
+        nv.cubin(prog, &cubin[0]);
+        nv.destroy(&prog);
+        mkdir((dir.substr(0, dir.rfind('/'))).c_str(), 0755);
+        mkdir(dir.c_str(), 0755);
+        const std::string tmp = base + ".tmp" + std::to_string((long long)getpid());
+        {
+            std::ofstream fc(tmp + ".cubin", std::ios::binary), fn(tmp + ".names");
+            fc.write(cubin.data(), (std::streamsize)cubin.size());
+            for (auto& l : lowered) fn << l << "\n";
+        }
+        std::rename((tmp + ".names").c_str(), (base + ".names").c_str());
+        std::rename((tmp + ".cubin").c_str(), (base + ".cubin").c_str());
+    }
+    if (why && why->empty()) *why = "compiled " + std::string(tag);
+    if (!load) return nullptr;
+    auto m = std::make_shared<JitModule>();
+    if (cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess) {
+        cudaGetLastError();
+        if (why) *why = "cudaLibraryLoadData failed";
+        return nullptr;
+    }
+    for (int i = 0; i < 4; ++i) {
+        cudaKernel_t k = nullptr;
+        if (cudaLibraryGetKernel(&k, m->lib, lowered[i].c_str()) != cudaSuccess) {
+            cudaGetLastError();
+            if (why) *why = "kernel " + lowered[i] + " not in the JIT library";
+            return nullptr;
+        }
+        m->kern[i] = (const void*)k;
+    }
+    void* dsm = nullptr;
+    size_t bytes = 0;
+    if (cudaLibraryGetGlobal(&dsm, &bytes, m->lib, "polar_jit_smem") != cudaSuccess || bytes != sizeof m->smem ||
+        cudaMemcpy(m->smem, dsm, sizeof m->smem, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        if (why) *why = "polar_jit_smem not readable";
+        return nullptr;
+    }
+    m->mask = mask;
+    m->schedule = jc.schedule;
+    RegistryEntry& e = m->entry;
+    e.name = "jit";
+    e.N = N;
+    e.K = K;
+    e.mask = m->mask.data();
+    e.hash = key.first;
+    e.n_ops = jc.n_ops;
+    e.warp_root = jc.warp_root;
+    Variant* vs[4] = {&e.tp_f32, &e.tp_i8, &e.lat_f32, &e.lat_i8};
+    for (int i = 0; i < 4; ++i)
+        *vs[i] = Variant{&m->kern[i], &m->smem[i], jc.vars[i].threads, jc.vars[i].frames, jc.vars[i].gscratch, jc.vars[i].extra};
+    e.xf_i8 = Variant{&m->none, &m->zero, 32, 1, 0, 0};  // no frame-interleaved kernel
+    e.xf_gslot = &m->zero;
+    e.mbox_i8 = Variant{nullptr, nullptr, 0, 0, 0, 0};
+    e.schedule = m->schedule.c_str();
+    g_jit_cache[key] = m;
+    return m;
+}
+
+}  // namespace
+
 // ------------------------------------------------------------------------- handle
 
 struct polar_code {
     uint32_t N = 0, K = 0;
     std::vector<uint8_t> mask;
     const RegistryEntry* entry = nullptr;  // specialised decoder, or nullptr: generic
+    std::shared_ptr<JitModule> jit;         // run-time specialised decoder (entry points into it)
+    std::string jit_note;                   // why an unregistered code kept the generic decoder
     std::vector<uint32_t> prog;             // generic decoder: the op program (tree.hpp)
     std::string sched;                      // Listing-1 op list
     uint32_t* d_prog = nullptr;
@@ -69,6 +278,7 @@ struct polar_code {
     int n_sm = 0;
     int occ[5] = {0, 0, 0, 0, 0};  // resident CTAs per SM: tp_f32, tp_i8, lat_f32, lat_i8, xf_i8
     int variant = 0;              // 0 auto, 1 throughput, 2 latency, 3 generic, 4 frame-interleaved
+    unsigned flags = 0;           // kernel flags: bit 0 = non-systematic output (polar_code_set_output)
     uint16_t* d_pos = nullptr;    // K information positions, ascending (encoder / generator)
     uint32_t* d_gtab = nullptr;   // gather table: info mask words, then info-bit prefix per word
     void* d_gscratch[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // per variant global stage scratch
@@ -160,6 +370,7 @@ static polar_status init_device(polar_code* h) {
     }
     for (int i = 0; i < (e ? 5 : 0); ++i) {
         const void* k = *vs[i]->kern;
+        if (!k) continue;  // a run-time specialised code has no frame-interleaved kernel
         CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*vs[i]->smem));
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &h->occ[i], k, (int)(vs[i]->threads * vs[i]->frames + vs[i]->extra), *vs[i]->smem));
@@ -248,12 +459,35 @@ extern "C" polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t*
     polar_code* h = new polar_code;
     h->N = N;
     h->K = K;
+    // POLAR_JIT_FORCE=1: ignore the build-time decoder (measures the run-time path on a code
+    // that has both)
+    if (const char* f = std::getenv("POLAR_JIT_FORCE"); f && f[0] == '1') e = nullptr;
+    if (!e) {  // no build-time decoder: specialise at run time (needs a device and NVRTC)
+        const char* env = std::getenv("POLAR_JIT");
+        const char* mx = std::getenv("POLAR_JIT_MAX_OPS");
+        const uint32_t max_ops = mx ? (uint32_t)std::strtoul(mx, nullptr, 10) : 4096u;
+        const uint32_t ops_fast = (uint32_t)schedule(build_tree((int)N, m.data())).size();
+        int count = 0;
+        if (env && env[0] == '0') h->jit_note = "POLAR_JIT=0";
+        else if (ops_fast > max_ops)  // compile time grows with the unrolled length
+            h->jit_note = std::to_string(ops_fast) + " Fast-SSC ops > POLAR_JIT_MAX_OPS=" + std::to_string(max_ops);
+        else if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            h->jit_note = "no CUDA device";
+        } else if ((h->jit = jit_build(N, K, m, &h->jit_note))) {
+            e = &h->jit->entry;
+        }
+    }
     h->mask = std::move(m);
     h->entry = e;  // nullptr: no specialised decoder, the generic (interpreted) one is used
     const Tree tree = build_tree((int)N, h->mask.data());
     const std::vector<std::string> ops = schedule(tree);
     h->n_ops = (uint32_t)ops.size();
     for (auto& o : ops) h->sched += o + ";";
+    if (e) {  // the specialised decoder's own op list (a build may use another node set, tree.hpp NodeSet)
+        h->n_ops = e->n_ops;
+        h->sched = e->schedule;
+    }
     h->prog = program(tree);  // the generic decoder serves unregistered codes and variant 3
     h->systematic_ok = superset_closed((int)N, h->mask.data());
     polar_status s = init_device(h);
@@ -288,6 +522,20 @@ extern "C" void polar_code_destroy(polar_code* h) {
     delete h;
 }
 
+extern "C" polar_status polar_jit_compile(uint32_t N, uint32_t K, const uint8_t* frozen_mask, char* log, uint32_t cap) {
+    if (!frozen_mask) return fail(POLAR_ERR_INVALID_ARGUMENT, "null mask");
+    if (N < 2 || N > 32768 || (N & (N - 1)) || K < 1 || K > N) return fail(POLAR_ERR_INVALID_ARGUMENT, "bad (N, K)");
+    std::vector<uint8_t> m(frozen_mask, frozen_mask + N);
+    for (auto& b : m) b = b ? 1 : 0;
+    std::string why;
+    jit_build(N, K, m, &why, false);
+    if (log && cap) {
+        std::strncpy(log, why.c_str(), cap - 1);
+        log[cap - 1] = 0;
+    }
+    return why.rfind("compiled ", 0) == 0 ? POLAR_OK : fail(POLAR_ERR_UNSUPPORTED_CODE, "%s", why.substr(0, 400).c_str());
+}
+
 extern "C" polar_status polar_code_query(const polar_code* h, uint32_t* N, uint32_t* K, uint32_t* n_ops,
                                          uint32_t* smem_bytes, uint32_t* warp_root) {
     if (!h) return fail(POLAR_ERR_INVALID_ARGUMENT, "null handle");
@@ -301,13 +549,21 @@ extern "C" polar_status polar_code_query(const polar_code* h, uint32_t* N, uint3
 
 extern "C" polar_status polar_code_is_specialised(const polar_code* h, int* specialised) {
     if (!h || !specialised) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
-    *specialised = h->entry != nullptr;
+    *specialised = h->jit ? 2 : h->entry != nullptr ? 1 : 0;
+    if (!h->entry && !h->jit_note.empty()) g_last_error = "generic decoder: " + h->jit_note;
     return POLAR_OK;
 }
 
 extern "C" polar_status polar_code_set_variant(polar_code* h, int variant) {
     if (!h || variant < 0 || variant > 4) return fail(POLAR_ERR_INVALID_ARGUMENT, "variant must be 0, 1, 2, 3 or 4");
     h->variant = variant;
+    return POLAR_OK;
+}
+
+extern "C" polar_status polar_code_set_output(polar_code* h, int mode) {
+    if (!h || (mode != POLAR_OUTPUT_SYSTEMATIC && mode != POLAR_OUTPUT_NONSYSTEMATIC))
+        return fail(POLAR_ERR_INVALID_ARGUMENT, "output mode must be POLAR_OUTPUT_SYSTEMATIC or POLAR_OUTPUT_NONSYSTEMATIC");
+    h->flags = mode == POLAR_OUTPUT_NONSYSTEMATIC ? 1u : 0u;
     return POLAR_OK;
 }
 
@@ -429,7 +685,8 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
         const uint32_t* gtab = h->d_gtab;
         const uint32_t* prog = h->d_prog;
         int nops = (int)h->prog.size(), N = (int)h->N, K = (int)h->K;
-        void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&prog, (void*)&nops, (void*)&N, (void*)&K};
+        unsigned fl = h->flags;
+        void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&prog, (void*)&nops, (void*)&N, (void*)&K, (void*)&fl};
         CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(32), args, sm, s));
         return POLAR_OK;
     }
@@ -441,7 +698,10 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     // Frame-interleaved variant (a lane per frame): forced by variant 4; automatic for int8
     // codes with N <= 1024 once the batch fills every SM with several 32-frame warps
     // (measured faster there only: (1024,512) 172 vs 146 Gbps; (2048,1723) 262 vs 316).
-    const bool xf = i8 && (h->variant == 4 || (h->variant == 0 && h->N <= 1024 && n >= (int64_t)h->n_sm * 32 * 4));
+    if (h->variant == 4 && h->flags) return fail(POLAR_ERR_UNSUPPORTED_CODE, "the frame-interleaved variant has systematic output only");
+    const bool has_xf = *e->xf_i8.kern != nullptr;
+    if (h->variant == 4 && i8 && !has_xf) return fail(POLAR_ERR_UNSUPPORTED_CODE, "no frame-interleaved kernel for this code");
+    const bool xf = i8 && has_xf && !h->flags && (h->variant == 4 || (h->variant == 0 && h->N <= 1024 && n >= (int64_t)h->n_sm * 32 * 4));
     if (xf) {  // 32 frames per warp, frames = warps per CTA
         const Variant& v = e->xf_i8;
         const int64_t groups = (n + 31) / 32;
@@ -470,9 +730,11 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     if (n > kDumpFrames) return fail(POLAR_ERR_INVALID_ARGUMENT, "POLAR_DEBUG_DUMP build: at most %d frames", (int)kDumpFrames);
     CUDA_TRY(cudaMemsetAsync(h->d_dump, 0xff, kDumpFrames * dump_stride(h->N) * sizeof(float), s));  // NaN
     float* dump = h->d_dump;
-    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs, (void*)&dump};
+    unsigned fl = h->flags;
+    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs, (void*)&fl, (void*)&dump};
 #else
-    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs};
+    unsigned fl = h->flags;
+    void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&gs, (void*)&fl};
 #endif
     return launch_with_scratch(h, vi, kern, dim3(grid), dim3(v.threads * v.frames + v.extra), args, smem, s);
 }
@@ -591,7 +853,8 @@ extern "C" polar_status polar_mailbox_open(polar_code* h, double idle_seconds) {
     unsigned long long idle_ns = (unsigned long long)(idle_seconds * 1e9);
     const uint32_t* gtab = h->d_gtab;
     int8_t* dbuf = h->mb.dbuf;
-    void* args[] = {&dframe, &dout, &dctl, &dbuf, (void*)&gtab, &idle_ns};
+    unsigned fl = h->flags;
+    void* args[] = {&dframe, &dout, &dctl, &dbuf, (void*)&gtab, &idle_ns, &fl};
     if ((e = cudaLaunchKernel(*v.kern, dim3(1), dim3(v.threads), args, *v.smem, h->mb.s)) != cudaSuccess) return bail("launch", e);
     h->mb.open = true;
     return POLAR_OK;

@@ -32,33 +32,42 @@ struct Tree {
     std::vector<Node> nodes;  // nodes[0] is the root
 };
 
+// Node sets of the decoder generator (the paper's algorithm ablation, tab:impl:tp:algo-unroll
+// P:948-963): Fast-SSC (default: Rate-0, Rate-1, Rep, SPC), the paper's
+// GPU set without SPC nodes, SSC (Rate-0 and Rate-1 nodes of any size)
+// and plain SC (no node specialisation: the traversal reaches every bit).
+enum class NodeSet : int { FastSSC = 0, NoSPC = 1, SSC = 2, SC = 3 };
+
 // Classify the constituent code frozen[off .. off+n): counts of frozen bits decide.
-inline Kind classify(const uint8_t* frozen, int off, int n) {
+inline Kind classify(const uint8_t* frozen, int off, int n, NodeSet set = NodeSet::FastSSC) {
     int n_frozen = 0;
     for (int i = off; i < off + n; ++i) n_frozen += frozen[i] != 0;
+    if (set == NodeSet::SC && n > 1) return Kind::Split;
     if (n_frozen == n) return Kind::Rate0;
     if (n_frozen == 0) return Kind::Rate1;
+    if (set == NodeSet::SSC) return Kind::Split;
     if (n_frozen == n - 1 && frozen[off + n - 1] == 0) return Kind::Rep;
+    if (set == NodeSet::NoSPC) return Kind::Split;
     if (n_frozen == 1 && frozen[off] != 0) return Kind::Spc;
     return Kind::Split;
 }
 
-inline int build_node(Tree& t, const uint8_t* frozen, int off, int n) {
+inline int build_node(Tree& t, const uint8_t* frozen, int off, int n, NodeSet set) {
     int id = (int)t.nodes.size();
-    t.nodes.push_back(Node{classify(frozen, off, n), n, off, -1, -1});
+    t.nodes.push_back(Node{classify(frozen, off, n, set), n, off, -1, -1});
     if (t.nodes[id].kind == Kind::Split) {
-        int l = build_node(t, frozen, off, n / 2);
-        int r = build_node(t, frozen, off + n / 2, n / 2);
+        int l = build_node(t, frozen, off, n / 2, set);
+        int r = build_node(t, frozen, off + n / 2, n / 2, set);
         t.nodes[id].left = l;
         t.nodes[id].right = r;
     }
     return id;
 }
 
-inline Tree build_tree(int N, const uint8_t* frozen) {
+inline Tree build_tree(int N, const uint8_t* frozen, NodeSet set = NodeSet::FastSSC) {
     Tree t;
     t.N = N;
-    build_node(t, frozen, 0, N);
+    build_node(t, frozen, 0, N, set);
     return t;
 }
 

@@ -101,8 +101,13 @@ def test_create_validation():
     with pytest.raises(pb.PolarError) as e:
         pb.PolarCode(48, 32, bad)  # N not a power of two
     assert e.value.status == pb.POLAR_ERR_INVALID_ARGUMENT
-    # a frozen set no decoder was specialised for gets the generic (interpreted) decoder
-    g = pb.PolarCode(64, 32, random_mask(999, 64, 32))
+    # a frozen set no decoder was specialised for gets the generic (interpreted) decoder when
+    # run-time specialisation is off (tests/test_jit.py covers it)
+    os.environ["POLAR_JIT"] = "0"
+    try:
+        g = pb.PolarCode(64, 32, random_mask(999, 64, 32))
+    finally:
+        del os.environ["POLAR_JIT"]
     assert not g.specialised
     assert g.schedule() == oracle.fastssc_trace(random_mask(999, 64, 32))
     assert pb.PolarCode(8, 5, np.array([1, 1, 0, 0, 1, 0, 0, 0], np.uint8)).specialised
@@ -171,3 +176,12 @@ def test_variant_and_mailbox_argument_checks_without_gpu():
             with pytest.raises(pb.PolarError) as e:
                 code.mailbox_open()
             assert e.value.status == pb.POLAR_ERR_CUDA
+
+
+def test_output_mode_argument_checks():
+    c = pb.PolarCode(8, 5, np.array([1, 1, 0, 0, 1, 0, 0, 0], np.uint8))
+    c.set_output("nonsystematic")
+    c.set_output("systematic")
+    with pytest.raises(pb.PolarError) as e:
+        pb._check(pb.lib().polar_code_set_output(c._h, 2))
+    assert e.value.status == pb.POLAR_ERR_INVALID_ARGUMENT

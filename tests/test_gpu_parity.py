@@ -120,10 +120,12 @@ GENERIC = [(2, 1, 301), (4, 2, 302), (8, 3, 303), (16, 9, 304), (32, 20, 305), (
 
 
 @pytest.mark.parametrize("N,K,seed", GENERIC, ids=[f"{n}_{k}" for n, k, _ in GENERIC])
-def test_generic_decoder_random_masks(N, K, seed):
-    """N1: frozen sets without a specialised decoder use the interpreted decoder."""
+def test_generic_decoder_random_masks(N, K, seed, monkeypatch):
+    """N1: frozen sets without a specialised decoder use the interpreted decoder (run-time
+    specialisation off: tests/test_jit.py covers it)."""
     from seeded_inputs import random_mask
 
+    monkeypatch.setenv("POLAR_JIT", "0")
     mask = random_mask(seed, N, K)
     code = pb.PolarCode(N, K, mask)
     assert not code.specialised
@@ -380,3 +382,31 @@ def test_bench_batches_every_frame_against_oracle(N, K, e, prof, n):
     x = llr.cpu().numpy()
     del llr
     assert_same(got, expected(mask, x), f"({N},{K}) {prof} x {n}")
+
+
+NONSYS = [c for c in CODES if c[1] in (8, 64, 1024, 2048, 4096, 32768)]
+
+
+@pytest.mark.parametrize("name,N,K,mask,ebn0", NONSYS, ids=[c[0] for c in NONSYS])
+@pytest.mark.parametrize("variant", ["throughput", "latency", "generic"])
+def test_nonsystematic_output_equals_oracle(name, N, K, mask, ebn0, variant):
+    """Non-systematic output mode (reading C4): u_hat[A] with u_hat = x_hat G_N.
+    Frames of the non-systematic code x = u G_N (u[A] = d, u[F] = 0); every frame
+    against the oracle's x_hat G_N, and noiseless frames return d exactly."""
+    code = pb.PolarCode(N, K, mask)
+    code.set_variant(variant)
+    code.set_output("nonsystematic")
+    n = _n_frames(N)
+    bits, noise = draw(4321, 0, n, K, N)
+    u = np.zeros((n, N), np.uint8)
+    u[:, mask == 0] = bits
+    x = oracle.encode(u)
+    llr = bpsk_awgn_llr(x, noise, ebn0 - 1.0, K)
+    for y in (llr, quantize_i8(llr)):
+        xh = oracle.fastssc_decode(mask, y, threads=THREADS)
+        want = oracle.pack_bits(oracle.info_bits(mask, oracle.encode(xh)))
+        assert_same(gpu_decode(code, y), want, f"{name} non-systematic {variant} {y.dtype}")
+    clean = np.where(x == 0, 8.0, -8.0).astype(np.float32)
+    np.testing.assert_array_equal(gpu_decode(code, clean), oracle.pack_bits(bits))
+    code.set_output("systematic")
+    assert_same(gpu_decode(code, clean), oracle.pack_bits(oracle.info_bits(mask, x)), f"{name} back to systematic")

@@ -412,3 +412,43 @@ def test_paper_memory_closed_forms():
     # P:1242 (tab:impl:power_vs_gal): 3,408 kB per stream on the K20c for 208 frames of the
     # (2048,1707) float decoder = 208 x (N input LLRs + N output values) x 4 bytes
     assert round(208 * (2048 + 2048) * 4 / 1000) == 3408
+
+
+@pytest.mark.parametrize("N,K,ebn0", [(16, 8, 2.0), (256, 128, 2.0), (1024, 512, 2.5)])
+def test_nonsystematic_information_is_uhat_on_a(N, K, ebn0):
+    """Non-systematic reading (C4): for x = u G_N with u[A] = d, u[F] = 0
+    (P:138-155), the decoded codeword mapped back by G_N (its own inverse) gives u_hat with
+    u_hat[A] = d and u_hat[F] = 0 on noiseless frames; SC's leaf decisions are that u_hat."""
+    frozen = oracle.construct_ga(N, K, ebn0)
+    bits, _ = si.draw(9, 0, 16, K, N)
+    u = np.zeros((16, N), np.uint8)
+    u[:, frozen == 0] = bits
+    x = oracle.encode(u)
+    llr = np.where(x == 0, 6.0, -6.0).astype(np.float32)
+    uh = oracle.encode(oracle.fastssc_decode(frozen, llr))
+    assert np.array_equal(uh[:, frozen == 0], bits) and not uh[:, frozen == 1].any()
+    _, us, _ = oracle.sc_decode(frozen, llr, with_stats=True)
+    assert np.array_equal(us, uh)
+
+
+@pytest.mark.parametrize("N,K,ebn0", [(64, 32, 2.0), (256, 128, 2.0), (1024, 700, 3.0)])
+def test_node_sets_of_the_ablation(N, K, ebn0):
+    """The ablation's node sets against what fixes them: the plain-SC
+    set reproduces O1 (recursive SC) exactly, int8 and f32, and visits every
+    bit (N leaves); on f32 frames without an exact-zero decision every set equals O1 (the
+    special-node rules are ML for their constituent codes, pin 5); the Fast-SSC set is O2."""
+    frozen = oracle.construct_ga(N, K, ebn0)
+    bits, noise = si.draw(21, 0, 48, K, N)
+    llr = si.bpsk_awgn_llr(oracle.encode_systematic(frozen, bits), noise, ebn0 - 1.5, K)
+    q = si.quantize_i8(llr)
+    assert np.array_equal(oracle.nodeset_decode(frozen, q, "sc"), oracle.sc_decode(frozen, q))
+    assert np.array_equal(oracle.nodeset_decode(frozen, llr, "sc"), oracle.sc_decode(frozen, llr))
+    assert np.array_equal(oracle.nodeset_decode(frozen, q, "fastssc"), oracle.fastssc_decode(frozen, q))
+    xs, _, zd = oracle.sc_decode(frozen, llr, with_stats=True)
+    keep = zd == 0
+    for s in ("nospc", "ssc"):
+        assert np.array_equal(oracle.nodeset_decode(frozen, llr, s)[keep], xs[keep]), s
+    tr = oracle.nodeset_trace(frozen, "sc")
+    assert sum(1 for t in tr if t == "Info<1>") == K  # every information bit is its own leaf
+    n_ops = [len(oracle.nodeset_trace(frozen, s)) for s in ("sc", "ssc", "nospc", "fastssc")]
+    assert n_ops == sorted(n_ops, reverse=True) and n_ops[-1] == len(oracle.fastssc_trace(frozen))
