@@ -36,6 +36,13 @@ void construct_ga(int N, int K, double design_ebn0_db, uint8_t* frozen);
 // generic.cu: the program-interpreted decoder for frozen sets without a specialised kernel
 const void* polar_generic_kernel(bool i8);
 int polar_generic_smem(bool i8, int N, int K);
+// ... and its long-code form (N > 32768): one CTA per frame, large stages in a global slot
+const void* polar_generic_big_kernel(bool i8);
+int polar_generic_big_smem(bool i8, int N);
+long long polar_generic_big_gslot_bytes(bool i8, int N);
+int polar_generic_big_threads();
+constexpr uint32_t kMaxUnrolledN = 32768;  // registry and run-time specialisation
+constexpr uint32_t kMaxN = 1u << 20;       // program-interpreted decoder
 
 using namespace polar;
 
@@ -269,7 +276,7 @@ struct polar_code {
     std::vector<uint32_t> prog;             // generic decoder: the op program (tree.hpp)
     std::string sched;                      // Listing-1 op list
     uint32_t* d_prog = nullptr;
-    int occ_generic[2] = {0, 0};
+    int occ_generic[2] = {0, 0};  // resident CTAs per SM of the generic decoder (f32, int8)
     uint32_t n_ops = 0;
     bool systematic_ok = false;  // information set closed under bit-superset (reading C4)
     // device side (absent when no usable device at create time)
@@ -279,16 +286,17 @@ struct polar_code {
     int occ[5] = {0, 0, 0, 0, 0};  // resident CTAs per SM: tp_f32, tp_i8, lat_f32, lat_i8, xf_i8
     int variant = 0;              // 0 auto, 1 throughput, 2 latency, 3 generic, 4 frame-interleaved
     unsigned flags = 0;           // kernel flags: bit 0 = non-systematic output (polar_code_set_output)
-    uint16_t* d_pos = nullptr;    // K information positions, ascending (encoder / generator)
+    uint32_t* d_pos = nullptr;    // K information positions, ascending (encoder / generator)
     uint32_t* d_gtab = nullptr;   // gather table: info mask words, then info-bit prefix per word
-    void* d_gscratch[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // per variant global stage scratch
-    size_t sc_bytes[5] = {0, 0, 0, 0, 0};  // its size (0: the variant needs none)
+    // per variant global stage scratch: tp_f32, tp_i8, lat_f32, lat_i8, xf_i8, long-code generic
+    void* d_gscratch[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t sc_bytes[6] = {0, 0, 0, 0, 0, 0};  // its size (0: the variant needs none)
     // Launches of one variant share its scratch slots: a launch on another stream waits for the
     // previous one (event), so concurrent decode calls on one handle stay correct.
     std::mutex sc_mu;
-    cudaEvent_t sc_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    cudaStream_t sc_last[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    bool sc_used[5] = {false, false, false, false, false};
+    cudaEvent_t sc_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t sc_last[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    bool sc_used[6] = {false, false, false, false, false, false};
     unsigned long long* d_trace = nullptr;  // POLAR_TRACE builds: per-op clock64 of the latency variant
     float* d_dump = nullptr;                // POLAR_DEBUG_DUMP builds: alpha stages of up to kDumpFrames frames
     uint32_t* d_info_mask = nullptr;  // N/32 words (>= 1), bit set = information position
@@ -349,13 +357,20 @@ static polar_status init_device(polar_code* h) {
     CUDA_TRY(cudaGetDevice(&h->device));
     CUDA_TRY(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
     const RegistryEntry* e = h->entry;
-    {  // generic decoder (any code): one warp per frame, all stages in shared memory
+    {  // generic decoder (any code): one warp per frame, all stages in shared memory; for
+       // N > 32768 one CTA per frame with the large stages in a global slot (allocated lazily)
+        const bool big = h->N > kMaxUnrolledN;
         for (int i = 0; i < 2; ++i) {
-            const void* k = polar_generic_kernel(i == 1);
-            const int sm = polar_generic_smem(i == 1, (int)h->N, (int)h->K);
+            const void* k = big ? polar_generic_big_kernel(i == 1) : polar_generic_kernel(i == 1);
+            const int sm = big ? polar_generic_big_smem(i == 1, (int)h->N) : polar_generic_smem(i == 1, (int)h->N, (int)h->K);
             CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ_generic[i], k, 32, sm));
+            CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->occ_generic[i], k, big ? polar_generic_big_threads() : 32, sm));
             if (h->occ_generic[i] < 1) return fail(POLAR_ERR_CUDA, "generic decoder cannot be resident");
+        }
+        if (big) {
+            h->sc_bytes[5] = (size_t)std::max(h->occ_generic[0], h->occ_generic[1]) * h->n_sm *
+                             (size_t)polar_generic_big_gslot_bytes(false, (int)h->N);
+            CUDA_TRY(cudaEventCreateWithFlags(&h->sc_ev[5], cudaEventDisableTiming));
         }
         CUDA_TRY(cudaMalloc(&h->d_prog, std::max<size_t>(1, h->prog.size()) * sizeof(uint32_t)));
         CUDA_TRY(cudaMemcpy(h->d_prog, h->prog.data(), h->prog.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
@@ -385,15 +400,15 @@ static polar_status init_device(polar_code* h) {
         if (h->sc_bytes[i] && i != 4) CUDA_TRY(cudaMalloc(&h->d_gscratch[i], h->sc_bytes[i]));
         if (h->sc_bytes[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->sc_ev[i], cudaEventDisableTiming));
     }
-    std::vector<uint16_t> pos;
+    std::vector<uint32_t> pos;
     std::vector<uint32_t> im(std::max<uint32_t>(1, h->N / 32), 0);
     for (uint32_t i = 0; i < h->N; ++i)
         if (!h->mask[i]) {
-            pos.push_back((uint16_t)i);
+            pos.push_back(i);
             im[i / 32] |= 1u << (i % 32);
         }
-    CUDA_TRY(cudaMalloc(&h->d_pos, pos.size() * sizeof(uint16_t)));
-    CUDA_TRY(cudaMemcpy(h->d_pos, pos.data(), pos.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMalloc(&h->d_pos, pos.size() * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemcpy(h->d_pos, pos.data(), pos.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     std::vector<uint32_t> gt(im);
     uint32_t acc = 0;
     for (uint32_t w : im) {
@@ -441,7 +456,7 @@ static polar_status init_device(polar_code* h) {
 extern "C" polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t* frozen_mask, polar_code** out) {
     if (!out || !frozen_mask) return fail(POLAR_ERR_INVALID_ARGUMENT, "null pointer");
     *out = nullptr;
-    if (N < 2 || N > 32768 || (N & (N - 1))) return fail(POLAR_ERR_INVALID_ARGUMENT, "N=%u is not a power of two in [2, 32768]", N);
+    if (N < 2 || N > kMaxN || (N & (N - 1))) return fail(POLAR_ERR_INVALID_ARGUMENT, "N=%u is not a power of two in [2, 2^20]", N);
     if (K < 1 || K > N) return fail(POLAR_ERR_INVALID_ARGUMENT, "K=%u not in [1, N]", K);
     std::vector<uint8_t> m(frozen_mask, frozen_mask + N);
     uint32_t nf = 0;
@@ -452,7 +467,7 @@ extern "C" polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t*
     if (nf != N - K) return fail(POLAR_ERR_INVALID_ARGUMENT, "mask has %u frozen bits, expected N-K=%u", nf, N - K);
     const uint64_t hsh = code_hash((int)N, (int)K, m.data());
     const RegistryEntry* e = nullptr;
-    for (uint32_t i = 0; i < kRegistrySize; ++i)
+    for (uint32_t i = 0; i < (N <= kMaxUnrolledN ? kRegistrySize : 0); ++i)
         if (kRegistry[i].hash == hsh && kRegistry[i].N == N && kRegistry[i].K == K &&
             std::memcmp(kRegistry[i].mask, m.data(), N) == 0)
             e = &kRegistry[i];
@@ -469,6 +484,7 @@ extern "C" polar_status polar_code_create(uint32_t N, uint32_t K, const uint8_t*
         const uint32_t ops_fast = (uint32_t)schedule(build_tree((int)N, m.data())).size();
         int count = 0;
         if (env && env[0] == '0') h->jit_note = "POLAR_JIT=0";
+        else if (N > kMaxUnrolledN) h->jit_note = "N > 32768: program-interpreted (P:1277)";
         else if (ops_fast > max_ops)  // compile time grows with the unrolled length
             h->jit_note = std::to_string(ops_fast) + " Fast-SSC ops > POLAR_JIT_MAX_OPS=" + std::to_string(max_ops);
         else if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
@@ -510,7 +526,7 @@ extern "C" void polar_code_destroy(polar_code* h) {
     if (h->d_pos) cudaFree(h->d_pos);
     if (h->d_info_mask) cudaFree(h->d_info_mask);
     if (h->d_gtab) cudaFree(h->d_gtab);
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < 6; ++i) {
         if (h->d_gscratch[i]) cudaFree(h->d_gscratch[i]);
         if (h->sc_ev[i]) cudaEventDestroy(h->sc_ev[i]);
     }
@@ -637,7 +653,7 @@ extern "C" polar_status polar_registry_entry(uint32_t i, uint32_t* N, uint32_t* 
 // launch of that variant when it was on another stream.  Under stream capture the ordering is
 // the caller's (an event recorded outside the capture cannot be waited on inside it).
 static polar_status launch_with_scratch(const polar_code* hc, int vi, const void* kern, dim3 grid, dim3 block,
-                                        void** args, unsigned smem, cudaStream_t s) {
+                                        void** args, unsigned smem, cudaStream_t s, int scratch_arg = 4) {
     polar_code* h = const_cast<polar_code*>(hc);
     if (!h->sc_bytes[vi]) {
         CUDA_TRY(cudaLaunchKernel(kern, grid, block, args, smem, s));
@@ -647,7 +663,7 @@ static polar_status launch_with_scratch(const polar_code* hc, int vi, const void
         std::lock_guard<std::mutex> lock(h->sc_mu);
         if (!h->d_gscratch[vi]) CUDA_TRY(cudaMalloc(&h->d_gscratch[vi], h->sc_bytes[vi]));
     }
-    args[4] = (void*)&h->d_gscratch[vi];
+    args[scratch_arg] = (void*)&h->d_gscratch[vi];
     // throughput variants with global stages: zero the frame-group counter (kernels.cuh DYN)
     const bool ctr = (POLAR_DYN && vi < 2) || vi == 4;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -678,15 +694,19 @@ static polar_status launch_decode(const polar_code* h, bool i8, const void* llr,
     if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device was available when the handle was created");
     const RegistryEntry* e = h->entry;
     if (!e || h->variant == 3) {  // generic decoder
-        const void* kern = polar_generic_kernel(i8);
-        const int sm = polar_generic_smem(i8, (int)h->N, (int)h->K);
+        const bool big = h->N > kMaxUnrolledN;
+        const void* kern = big ? polar_generic_big_kernel(i8) : polar_generic_kernel(i8);
+        const int sm = big ? polar_generic_big_smem(i8, (int)h->N) : polar_generic_smem(i8, (int)h->N, (int)h->K);
         const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)h->occ_generic[i8 ? 1 : 0] * h->n_sm);
         long long nn = (long long)n;
         const uint32_t* gtab = h->d_gtab;
         const uint32_t* prog = h->d_prog;
         int nops = (int)h->prog.size(), N = (int)h->N, K = (int)h->K;
         unsigned fl = h->flags;
-        void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&prog, (void*)&nops, (void*)&N, (void*)&K, (void*)&fl};
+        void* gslot = nullptr;
+        void* args[] = {(void*)&llr, (void*)&nn, (void*)&out, (void*)&gtab, (void*)&prog, (void*)&nops, (void*)&N, (void*)&K,
+                        (void*)&fl, (void*)&gslot};
+        if (big) return launch_with_scratch(h, 5, kern, dim3(grid), dim3(polar_generic_big_threads()), args, sm, s, 9);
         CUDA_TRY(cudaLaunchKernel(kern, dim3(grid), dim3(32), args, sm, s));
         return POLAR_OK;
     }
@@ -941,12 +961,18 @@ __device__ void transform_smem(uint32_t* x, int N, int nw) {
 }
 
 // Systematic codeword in smem from packed info bits (reading C4): v[A] = d, x = mask_A(vG) G.
-__device__ void systematic_smem(uint32_t* x, const uint32_t* info, const uint16_t* pos, const uint32_t* info_mask,
+// info_word(q) yields information word q (32 bits, LSB-first); each thread places the set bits
+// of its words at their positions pos[] (uint32: N up to 2^20).
+template <class InfoWord>
+__device__ void systematic_smem(uint32_t* x, InfoWord info_word, const uint32_t* pos, const uint32_t* info_mask,
                                 int N, int K, int nw) {
     for (int k = threadIdx.x; k < nw; k += blockDim.x) x[k] = 0;
     __syncthreads();
-    for (int t = threadIdx.x; t < K; t += blockDim.x)
-        if ((info[t >> 5] >> (t & 31)) & 1u) atomicOr(&x[pos[t] >> 5], 1u << (pos[t] & 31));
+    for (int q = threadIdx.x; q < (K + 31) / 32; q += blockDim.x)
+        for (uint32_t w = info_word(q); w; w &= w - 1) {
+            const uint32_t t = pos[32 * q + __ffs(w) - 1];
+            atomicOr(&x[t >> 5], 1u << (t & 31));
+        }
     __syncthreads();
     transform_smem(x, N, nw);
     for (int k = threadIdx.x; k < nw; k += blockDim.x) x[k] &= info_mask[k];
@@ -954,37 +980,38 @@ __device__ void systematic_smem(uint32_t* x, const uint32_t* info, const uint16_
     transform_smem(x, N, nw);
 }
 
-__global__ void k_encode(const uint32_t* info, long long n, uint32_t* cw, const uint16_t* pos,
+__global__ void k_encode(const uint32_t* info, long long n, uint32_t* cw, const uint32_t* pos,
                          const uint32_t* info_mask, int N, int K) {
     extern __shared__ uint32_t x[];
     const int nw = N >= 32 ? N / 32 : 1;
     const int wk = (K + 31) / 32;
     for (long long f = blockIdx.x; f < n; f += gridDim.x) {
-        systematic_smem(x, info + f * wk, pos, info_mask, N, K, nw);
+        const uint32_t* d = info + f * wk;
+        systematic_smem(x, [&](int q) { return d[q]; }, pos, info_mask, N, K, nw);
         for (int k = threadIdx.x; k < nw; k += blockDim.x) cw[f * nw + k] = x[k];
         __syncthreads();
     }
 }
 
 __global__ void k_gen(unsigned long long seed, unsigned long long first, long long n, float sigma, float llr_scale,
-                      float q_scale, float* llr_f32, int8_t* llr_i8, uint32_t* info_out, const uint16_t* pos,
+                      float q_scale, float* llr_f32, int8_t* llr_i8, uint32_t* info_out, const uint32_t* pos,
                       const uint32_t* info_mask, int N, int K) {
     extern __shared__ uint32_t sm[];
     const int nw = N >= 32 ? N / 32 : 1;
     const int wk = (K + 31) / 32;
     uint32_t* x = sm;
-    uint32_t* info = sm + nw;
     const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
     for (long long f = blockIdx.x; f < n; f += gridDim.x) {
         const unsigned long long g = first + (unsigned long long)f;
-        for (int q = threadIdx.x; q < wk; q += blockDim.x) {
+        // information word q of frame g: Philox keyed by the seed, counter (g, q) (reading C6)
+        auto info_word = [&](int q) {
             uint32_t w = philox(U4{(uint32_t)g, (uint32_t)(g >> 32), (uint32_t)q, 0xB17u}, k0, k1).x;
             if (q == wk - 1 && (K & 31)) w &= (1u << (K & 31)) - 1u;
-            info[q] = w;
-            if (info_out) info_out[f * wk + q] = w;
-        }
-        __syncthreads();
-        systematic_smem(x, info, pos, info_mask, N, K, nw);
+            return w;
+        };
+        if (info_out)
+            for (int q = threadIdx.x; q < wk; q += blockDim.x) info_out[f * wk + q] = info_word(q);
+        systematic_smem(x, info_word, pos, info_mask, N, K, nw);
         // BPSK 0 -> +1, 1 -> -1; y = s + sigma n; LLR = 2 y / sigma^2 (readings C6/C7).
         for (int q4 = threadIdx.x; q4 < (N + 3) / 4; q4 += blockDim.x) {
             const U4 r = philox(U4{(uint32_t)g, (uint32_t)(g >> 32), (uint32_t)q4, 0xA3Cu}, k0, k1);
@@ -1048,6 +1075,7 @@ extern "C" polar_status polar_encode_systematic(const polar_code* h, const uint3
     if (!h->dev_ready) return fail(POLAR_ERR_CUDA, "no CUDA device");
     const int nw = h->N >= 32 ? h->N / 32 : 1;
     const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)h->n_sm * 16);
+    if (nw * 4 > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, nw * 4));
     k_encode<<<grid, 256, nw * 4, (cudaStream_t)stream>>>(info, (long long)n, cw, h->d_pos, h->d_info_mask, (int)h->N,
                                                           (int)h->K);
     CUDA_TRY(cudaGetLastError());
@@ -1066,9 +1094,9 @@ extern "C" polar_status polar_gen_bpsk_awgn(const polar_code* h, uint64_t seed, 
     const double rate = (double)h->K / (double)h->N;
     const double sigma2 = 1.0 / (2.0 * rate * std::pow(10.0, ebn0_db / 10.0));
     const int nw = h->N >= 32 ? h->N / 32 : 1;
-    const int wk = (int)words_of(h->K);
     const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)h->n_sm * 16);
-    k_gen<<<grid, 256, (nw + wk) * 4, (cudaStream_t)stream>>>(
+    if (nw * 4 > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(k_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, nw * 4));
+    k_gen<<<grid, 256, nw * 4, (cudaStream_t)stream>>>(
         (unsigned long long)seed, (unsigned long long)first_frame, (long long)n, (float)std::sqrt(sigma2),
         (float)(2.0 / sigma2), q_scale, llr_f32, llr_i8, info, h->d_pos, h->d_info_mask, (int)h->N, (int)h->K);
     CUDA_TRY(cudaGetLastError());
