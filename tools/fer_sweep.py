@@ -29,6 +29,42 @@ import paper_1504_00353_b200 as pb  # noqa: E402
 SEED = 1504000353
 
 
+# ------------------------------------------------------------------ checkpoint / resume
+# Every finished point is one JSON line; with --out FILE the lines are also appended (and
+# flushed) to FILE, and --resume skips the points FILE already holds, so a sweep cut off by a
+# time limit (the FER-1e-8 points take GPU-hours) restarts where it stopped.
+_OUT = None
+
+
+def point_key(d):
+    """Identity of a finished point: (code, design, Eb/N0, profile[, first frame, frame cap])."""
+    k = (tuple(d["code"]), float(d["design_ebn0"]), float(d["ebn0"]), d["profile"])
+    return k + ((int(d["first_frame"]), int(d.get("max_frames", d["frames"]))) if "first_frame" in d else ())
+
+
+def completed(path):
+    done = set()
+    if path and os.path.exists(path):
+        for line in open(path):
+            line = line.strip()
+            if line.startswith("{"):
+                try:
+                    done.add(point_key(json.loads(line)))
+                except (KeyError, ValueError):
+                    pass
+    return done
+
+
+def emit(d):
+    line = json.dumps(d)
+    print(line, flush=True)
+    if _OUT:
+        with open(_OUT, "a") as f:
+            f.write(line + "\n")
+            f.flush()
+            os.fsync(f.fileno())
+
+
 def clopper_pearson(k, n, a=0.05):
     lo = 0.0 if k == 0 else beta_dist.ppf(a / 2, k, n - k + 1)
     hi = 1.0 if k == n else beta_dist.ppf(1 - a / 2, k + 1, n - k)
@@ -53,8 +89,12 @@ def fer(a):
     truth = torch.empty(chunk, W, dtype=torch.int32, device="cuda")
     out = torch.empty(chunk, W, dtype=torch.int32, device="cuda")
     rng = np.random.default_rng(7)
+    done = completed(a.out) if a.resume else set()
     for e in [float(x) for x in a.points.split(",")]:
         for prof in (["i8", "f32"] if a.f32 else ["i8"]):
+            if ((N, K), a.design, e, prof) in done:
+                print(f"resume: skipping ({N},{K}) {e} dB {prof}", file=sys.stderr)
+                continue
             frames = bit_err = frame_err = checked = 0
             first = 0
             t0 = time.time()
@@ -79,10 +119,10 @@ def fer(a):
                 frames += n
                 first += n
             lo, hi = clopper_pearson(frame_err, frames)
-            print(json.dumps({"code": [N, K], "design_ebn0": a.design, "ebn0": e, "profile": prof, "frames": frames,
-                              "frame_errors": frame_err, "fer": frame_err / frames, "fer_ci95": [lo, hi],
-                              "ber": bit_err / (frames * K), "ga_fer": ga_fer(N, K, a.design, e),
-                              "oracle_checked_frames": checked, "seconds": round(time.time() - t0, 2)}), flush=True)
+            emit({"code": [N, K], "design_ebn0": a.design, "ebn0": e, "profile": prof, "frames": frames,
+                  "frame_errors": frame_err, "fer": frame_err / frames, "fer_ci95": [lo, hi],
+                  "ber": bit_err / (frames * K), "ga_fer": ga_fer(N, K, a.design, e),
+                  "oracle_checked_frames": checked, "seconds": round(time.time() - t0, 2)})
 
 
 def ferfast(a):
@@ -97,6 +137,9 @@ def ferfast(a):
     chunk = a.chunk
     e = float(a.points)
     prof = "f32" if a.f32 else "i8"
+    if a.resume and ((N, K), a.design, e, prof, a.first_frame, a.max_frames) in completed(a.out):
+        print(f"resume: segment ({N},{K}) {e} dB {prof} from frame {a.first_frame} already done", file=sys.stderr)
+        return
     x = torch.empty(chunk, N, dtype=torch.float32 if a.f32 else torch.int8, device="cuda")
     truth = torch.empty(chunk, W, dtype=torch.int32, device="cuda")
     out = torch.empty(chunk, W, dtype=torch.int32, device="cuda")
@@ -133,10 +176,9 @@ def ferfast(a):
         frames += n
     torch.cuda.synchronize()
     f_, be, fe = ctr.tolist()
-    print(json.dumps({"code": [N, K], "design_ebn0": a.design, "ebn0": e, "profile": prof,
-                      "first_frame": a.first_frame, "frames": f_, "frame_errors": fe, "bit_errors": be,
-                      "error_frames": err_frames, "oracle_checked_frames": checked,
-                      "seconds": round(time.time() - t0, 1)}), flush=True)
+    emit({"code": [N, K], "design_ebn0": a.design, "ebn0": e, "profile": prof,
+          "first_frame": a.first_frame, "frames": f_, "max_frames": a.max_frames, "frame_errors": fe, "bit_errors": be,
+          "error_frames": err_frames, "oracle_checked_frames": checked, "seconds": round(time.time() - t0, 1)})
 
 
 def batch(a):
@@ -213,5 +255,8 @@ if __name__ == "__main__":
     ap.add_argument("--check", type=int, default=64)
     ap.add_argument("--f32", action="store_true")
     ap.add_argument("--max-log4", type=int, default=8)
+    ap.add_argument("--out", default=None, help="also append every finished point to this JSON-lines file")
+    ap.add_argument("--resume", action="store_true", help="skip the points --out already holds")
     a = ap.parse_args()
+    _OUT = a.out
     {"fer": fer, "ferfast": ferfast, "batch": batch, "idud": idud}[a.mode](a)

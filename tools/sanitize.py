@@ -31,12 +31,37 @@ for N, K, e in CASES:
             bad += not ok
             print(f"({N},{K}) {variant:10s} {prof}: {'ok' if ok else 'MISMATCH'}", flush=True)
 m = random_mask(5, 256, 100)
+os.environ["POLAR_JIT"] = "0"  # the generic decoder itself
 code = pb.PolarCode(256, 100, m)
+del os.environ["POLAR_JIT"]
 x = random_llr_i8(9, (5, 256))
 ok = np.array_equal(code.decode_i8(torch.from_numpy(x).cuda()).cpu().numpy().view(np.uint32),
                     oracle.pack_bits(oracle.info_bits(m, oracle.fastssc_decode(m, x))))
 bad += not ok
 print("generic random mask:", "ok" if ok else "MISMATCH")
+# round 2: non-systematic output, a run-time specialised code, a long code (N > 32768)
+for N, K, e in [(2048, 1723, 4.0), (32768, 29492, 4.5)]:
+    mask = oracle.construct_ga(N, K, e)
+    code = pb.PolarCode(N, K, mask)
+    code.set_output("nonsystematic")
+    x = random_llr_i8(N + 3, (5, N), -60, 60)
+    want = oracle.pack_bits(oracle.info_bits(mask, oracle.encode(oracle.fastssc_decode(mask, x))))
+    for variant in ("throughput", "latency", "generic"):
+        code.set_variant(variant)
+        ok = np.array_equal(code.decode_i8(torch.from_numpy(x).cuda()).cpu().numpy().view(np.uint32), want)
+        bad += not ok
+        print(f"({N},{K}) {variant:10s} non-systematic: {'ok' if ok else 'MISMATCH'}", flush=True)
+for N, K, e in [(4096, 2048, 3.0), (65536, 58982, 4.5)]:
+    mask = oracle.construct_ga(N, K, e)
+    code = pb.PolarCode(N, K, mask)
+    x = random_llr_i8(N + 5, (3, N), -60, 60)
+    want = oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, x)))
+    for prof, v in (("i8", x), ("f32", x.astype(np.float32))):
+        t = torch.from_numpy(v).cuda()
+        ok = np.array_equal((code.decode_i8(t) if prof == "i8" else code.decode_f32(t)).cpu().numpy().view(np.uint32), want)
+        bad += not ok
+        kind = "run-time specialised" if code.run_time_specialised else "long-code generic"
+        print(f"({N},{K}) {kind} {prof}: {'ok' if ok else 'MISMATCH'}", flush=True)
 # batch-1 mailbox (persistent kernel on host-mapped memory)
 for N, K, e in [(2048, 1723, 4.0), (32768, 29492, 4.5)]:
     mask = oracle.construct_ga(N, K, e)
