@@ -56,6 +56,8 @@ struct Spec {
     int gs = -1;          // stages of size >= gs live in global scratch in the throughput variant
     int h16 = 0;          // int8 throughput variant: stages of size <= h16 stored as f16 (H16=; 0: none)
     NodeSet nodes = NodeSet::FastSSC;  // NODES=fastssc|nospc|ssc|sc: the algorithm ablation (tree.hpp)
+    bool repspc = false;  // speculative RepSPC nodes in the warp subtrees (REPSPC=1; measured
+                          // neutral for batch-1 latency and -2% throughput at N = 32768: opt-in)
     int xsm = 48 * 1024;  // frame-interleaved variant: shared-memory budget per warp (XSM=; 24K/48K/72K
                           // measured 162/262/207 Gbps at (2048,1723), profiles/r1_history.md)
     int xwpc = 1;         // frame-interleaved variant: warps per CTA (XWPC=)
@@ -76,6 +78,7 @@ struct TraceMarks {
 };
 TraceMarks* g_marks = nullptr;
 int g_ll = 0;  // lane-local threshold of the code being emitted
+bool g_repspc = true;  // speculative RepSPC for the code being emitted
 
 struct SharedFns {
     const std::vector<uint8_t>& mask;
@@ -211,6 +214,12 @@ struct Emitter {
         // children read the register stage `child`
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
+        if (g_repspc && n >= 4 && n <= 32 && l.kind == Kind::Rep && r.kind == Kind::Spc) {
+            std::string m = mask_name();  // speculative RepSPC, one fused op
+            o << ind << "const uint32_t " << m << " = wRepSPCm<P, " << N_ << ">(" << src << ");\n";
+            mk("RepSPC<" + N_ + ">");
+            return m;
+        }
         if (l.kind == Kind::Rate0) {
             o << ind << "wG0R<P, " << N_ << ">(" << src << ", " << child << ");\n";
             mk("G_0R<" + N_ + ">");
@@ -398,11 +407,11 @@ struct CtaEmitter {
             g_marks = keep;
             emit_warp_sub(subs, t, id, fname + "_lat", sh_lat ? sh_lat : sh, false, helper || latni);
             lat_subs.push_back(fname + "_lat");
-            emit("if constexpr (T == 32) { " + fname + "_tp<P>(" + src + ", beta); } else { if (gtid<T>() < 32) " +
+            emit("if constexpr (T == 32) { " + fname + "_tp<P>(" + src + ", beta); } else { if (w0) " +
                  fname + "_lat<P>(" + src + ", beta); }");
         } else {
             emit_warp_sub(subs, t, id, fname, sh);
-            emit("if (gtid<T>() < 32) " + fname + "<P>(" + src + ", beta);");
+            emit("if (w0) " + fname + "<P>(" + src + ", beta);");
         }
         emit("sync();");
     }
@@ -414,7 +423,7 @@ struct CtaEmitter {
         const Node& v = t.nodes[id];
         if (v.kind == Kind::Rate0) return;  // beta zeroed at frame start
         if (v.n > W && v.n <= XW && !in_region) {
-            emit_raw("if (gtid<T>() < 32) {  // warp-0 region");
+            emit_raw("if (w0) {  // warp-0 region");
             in_region = true;
             cta(id, src);
             in_region = false;
@@ -676,6 +685,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     TraceMarks marks;
     g_marks = &marks;
     g_ll = sp.ll;
+    g_repspc = sp.repspc;
     marks.mark("start");
     std::ostringstream o;
     // One struct per warp-subtree size: "Code" (throughput variants) and, when WLAT differs,
@@ -746,6 +756,11 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
           << "    static PD_INLINE void decode(const ChanT* chan, typename P::st_t* stages, typename P::st_t* gst,\n"
           << "                                 typename P::v_t* wst, uint32_t* beta, const SyncT& sync) {\n"
           << "        constexpr bool NI = T == 32 && N >= 8192;  // shared non-inlined stage ops\n"
+          << "        // warp 0 of the group, as a value the compiler knows is warp-uniform (a shuffle from\n"
+          << "        // lane 0): the subtree code it guards then needs no WARPSYNC.COLLECTIVE wrappers\n"
+          << "        // around its shuffles/votes (threadIdx.x < 32 would, measured in the SASS)\n"
+          << "        const bool w0 = T == 32 || __shfl_sync(FULL, threadIdx.x >> 5, 0) == 0;\n"
+          << "        (void)w0;\n"
           << "        PTRACE(0);\n"
           << body.str() << "    }\n";
     }
@@ -994,6 +1009,7 @@ void parse_options(Spec& sp, std::istream& ls) {
             else if (opt.rfind("FPC=", 0) == 0) sp.fpc_max = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("GS=", 0) == 0) sp.gs = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("H16=", 0) == 0) sp.h16 = std::atoi(opt.c_str() + 4);
+            else if (opt.rfind("REPSPC=", 0) == 0) sp.repspc = std::atoi(opt.c_str() + 7) != 0;
             else if (opt.rfind("NODES=", 0) == 0) {
                 const std::string v = opt.substr(6);
                 sp.nodes = v == "sc" ? NodeSet::SC : v == "ssc" ? NodeSet::SSC : v == "nospc" ? NodeSet::NoSPC : NodeSet::FastSSC;

@@ -658,6 +658,35 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
     bw |= hb << s0;
 }
 
+// RepSPC<n>: a node whose left child is a repetition code and right child an SPC
+// code, decoded speculatively as the paper describes -- the repetition code and two instances
+// of the SPC code, one assuming the repetition output is all 0's and the other all 1's, run
+// side by side, and the repetition decision selects.  Bit-identical to the composition
+// F<n>, Repetition<n/2>, G<n>, SPC<n/2>, Combine<n> (same f/g arithmetic, operands and sum
+// order); the G with beta = 1 is b - a, with beta = 0 b + a.  Replicated nodes (n <= 32).
+template <class P, int n, class Src>
+PD_INLINE uint32_t wRepSPCm(const Src& s) {
+    static_assert(n >= 4 && n <= 32, "");
+    constexpr int h = n / 2;
+    using V = typename P::v_t;
+    V x, y;
+    s.pair(h, x, y);  // own element (lane mod n) and the partner (xor h)
+    V cf[1] = {P::f(x, y)};  // F: the left child, replicated (lane holds element lane mod h)
+    PD_DUMPR(n, cf);
+    const bool second = lane_id() & h;  // lanes holding alpha[i + h]
+    const V a = second ? y : x, b = second ? x : y;
+    V g0[1] = {P::g0(a, b)}, g1[1] = {P::g(a, b, 1u)};  // G for beta_l = 0 and 1
+    const uint32_t m0 = wSPCm<P, h>(RegSrc<P>{g0});
+    const uint32_t m1 = wSPCm<P, h>(RegSrc<P>{g1});
+    const bool r = wRepDecide<P, h>(RegSrc<P>{cf});  // the repetition decision selects
+#ifdef POLAR_DEBUG_DUMP
+    V gs[1] = {r ? g1[0] : g0[0]};
+    PD_DUMPR(n, gs);
+#endif
+    const uint32_t ml = r ? low_mask(h) : 0u, mr = r ? m1 : m0;
+    return (ml ^ mr) | (mr << h);
+}
+
 // ------------------------------------------------------- lane-local tiny subtrees (n <= 16)
 // A split node of a few elements is decoded inside every lane: its n values (replicated, lane
 // k holds element k) are gathered once with n independent shuffles, then the whole subtree

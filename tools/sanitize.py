@@ -55,8 +55,8 @@ for N, K, e in [(4096, 2048, 3.0), (65536, 58982, 4.5)]:
     mask = oracle.construct_ga(N, K, e)
     code = pb.PolarCode(N, K, mask)
     x = random_llr_i8(N + 5, (3, N), -60, 60)
-    want = oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, x)))
     for prof, v in (("i8", x), ("f32", x.astype(np.float32))):
+        want = oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, v)))  # per profile (int8 saturates)
         t = torch.from_numpy(v).cuda()
         ok = np.array_equal((code.decode_i8(t) if prof == "i8" else code.decode_f32(t)).cpu().numpy().view(np.uint32), want)
         bad += not ok

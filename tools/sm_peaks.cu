@@ -102,6 +102,45 @@ __global__ void k_lds(uint32_t seed, uint32_t* out, unsigned long long* clk) {
     }
 }
 
+// dependent-chain latency: one warp, one chain, ITERS ops; cycles per op by clock64
+template <int K>
+__global__ void k_lat(uint32_t seed, uint32_t* out, unsigned long long* clk) {
+    uint32_t x = seed * (threadIdx.x + 1);
+    const uint32_t y = seed ^ 0x3c003c00u;
+    __shared__ uint32_t sm[64];
+    sm[threadIdx.x] = threadIdx.x;
+    __syncwarp();
+    const uint64_t c0 = clock64();
+#pragma unroll 1
+    for (int i = 0; i < ITERS / 16; ++i)
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {  // 16 dependent ops per trip: the loop overhead is amortised
+        if constexpr (K == 100) x = (uint32_t)__shfl_xor_sync(0xffffffffu, (int)x, 1) + 1u;  // SHFL + IADD
+        else if constexpr (K == 101) x = __ballot_sync(0xffffffffu, (x & (1u << (threadIdx.x & 31))) != 0) + 1u;
+        else if constexpr (K == 102) x = __reduce_min_sync(0xffffffffu, x) + threadIdx.x;
+        else if constexpr (K == 103) x = __float_as_uint(__fadd_rn(__uint_as_float(x), 1.0f));
+        else if constexpr (K == 104) x = sm[x & 31] + 1u;  // LDS (dependent address)
+        else if constexpr (K == 105) { asm volatile("bar.sync 1, 512;" ::: "memory"); x += 1u; }
+        else x = op<K>(x, y);
+    }
+    const uint64_t c1 = clock64();
+    if (x == seed) out[threadIdx.x] = x;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        clk[0] = c1 - c0;
+        clk[1] = 0;
+    }
+}
+
+template <int K>
+static int lat(const char* name, uint32_t* out, unsigned long long* dclk, int threads, bool last) {
+    k_lat<K><<<1, threads>>>(12345u, out, dclk);
+    CK(cudaDeviceSynchronize());
+    unsigned long long clk[2];
+    CK(cudaMemcpy(clk, dclk, sizeof clk, cudaMemcpyDeviceToHost));
+    printf("    \"%s\": %.1f%s\n", name, (double)clk[0] / ITERS, last ? "" : ",");
+    return 0;
+}
+
 template <class Kern>
 static int run(const char* name, Kern kern, int nsm, uint32_t* out, unsigned long long* dclk, double per_thread_ops,
                const char* unit, bool last) {
@@ -157,6 +196,15 @@ int main() {
     run("SHF", k_pipe<11>, nsm, out, clk, ops, "lane-ops", false);
     run("HFMA2", k_pipe<12>, nsm, out, clk, ops, "lane-ops", false);
     run("LDS128", k_lds, nsm, out, clk, ops * 16.0, "B", true);
+    printf("  },\n  \"latency_cycles_per_dependent_op\": {\n");
+    lat<100>("SHFL+IADD", out, clk, 32, false);
+    lat<101>("VOTE.ballot+IADD", out, clk, 32, false);
+    lat<102>("REDUX.min+IADD", out, clk, 32, false);
+    lat<103>("FADD", out, clk, 32, false);
+    lat<4>("FMNMX", out, clk, 32, false);
+    lat<0>("LOP3", out, clk, 32, false);
+    lat<104>("LDS+IADD", out, clk, 32, false);
+    lat<105>("bar.sync 512 threads+IADD", out, clk, 512, true);
     printf("  }\n}\n");
     return 0;
 }
