@@ -67,6 +67,15 @@ PD_INLINE uint32_t h2max(uint32_t a, uint32_t b) {
 
 PD_INLINE unsigned lane_id() { return threadIdx.x & 31u; }
 
+template <class A, class B>
+struct same_t {
+    static constexpr bool value = false;
+};
+template <class A>
+struct same_t<A, A> {
+    static constexpr bool value = true;
+};
+
 // POLAR_TRACE builds: clock64() after every op of the latency variant's critical path, block 0
 // thread 0 only, into the buffer the library passes (tools/trace_latency.py reads it back).
 #ifdef POLAR_TRACE
@@ -113,6 +122,7 @@ PD_INLINE void dump_reg(const V* c) {
 }
 PD_INLINE float dump_val(float x) { return x; }
 PD_INLINE float dump_val(int8_t x) { return (float)x; }
+PD_INLINE float dump_val(uint8_t x) { return (float)((int)x - 128); }  // biased int8 stage
 PD_INLINE float dump_val(__half x) { return __half2float(x); }
 // a stage written by a CTA-scope op: h elements at p (group of T threads)
 template <int T, class S>
@@ -174,9 +184,13 @@ struct PF32 {
 // int8 profile: 8-bit storage (channel and shared-memory stages); registers hold the same
 // integers as f32, which is exact here (|values| <= 254 in any single g, sums < 2^24), so
 // f is one FMNMX with |.| modifiers plus the sign, and g one FADD plus the clamp.
+// Stages written by the decoder hold v + 128 as an unsigned byte ("biased"): the f16x2 unpack
+// (0x64tt = 1024 + t) and pack then need no sign-bias XOR, one ALU-pipe instruction less per 4
+// values each way (the ALU pipe is the kernel's busiest unit, profiles/r2k_tp32k.txt).  The
+// channel stays signed int8 as the API defines it.
 struct PI8 {
     using in_t = int8_t;
-    using st_t = int8_t;
+    using st_t = uint8_t;
     using v_t = float;
     using acc_t = float;
     static constexpr bool kExactSum = true;  // integer sums below 2^24: any order is exact (C12)
@@ -184,7 +198,8 @@ struct PI8 {
     static constexpr bool kChanInSmem = true;
     // -128 -> -127 (C8); int -> float by the exponent trick (integer ALU + one FADD)
     static PD_INLINE v_t ld(int8_t x) { return __int_as_float(0x4B400000 + max((int)x, -127)) - 12582912.0f; }
-    static PD_INLINE int8_t st(v_t x) { return (int8_t)__float2int_rn(x); }
+    static PD_INLINE uint8_t st(v_t x) { return (uint8_t)(__float2int_rn(x) + 128); }
+    static PD_INLINE v_t ld(uint8_t t) { return __int_as_float(0x4B400000 + (int)t) - 12583040.0f; }  // biased stage
     static PD_INLINE v_t ld(float x) { return x; }  // the f32 subtree-input stage
     static PD_INLINE v_t ld(__half x) { return __half2float(x); }  // f16 stages (exact integers)
     static PD_INLINE v_t f(v_t a, v_t b) { return PF32::f(a, b); }
@@ -318,10 +333,11 @@ template <int CE>
 struct Chunk<PI8, CE> {
     static_assert(CE == 4 || CE == 8 || CE == 16, "");
     uint32_t h[CE / 2];
-    PD_INLINE void unpack(const uint32_t* w, bool clamp) {
+    // biased: stage bytes already hold v + 128 (PI8); else the signed channel (bias by XOR)
+    PD_INLINE void unpack(const uint32_t* w, bool clamp, bool biased = false) {
 #pragma unroll
         for (int q = 0; q < CE / 4; ++q) {
-            const uint32_t t = w[q] ^ 0x80808080u;
+            const uint32_t t = biased ? w[q] : w[q] ^ 0x80808080u;
             h[2 * q] = h2add(__byte_perm(t, 0x64646464u, 0x4140), 0xE480E480u);
             h[2 * q + 1] = h2add(__byte_perm(t, 0x64646464u, 0x4342), 0xE480E480u);
             if (clamp) {  // channel input: -128 -> -127 (reading C8)
@@ -349,7 +365,7 @@ struct Chunk<PI8, CE> {
     }
     template <class S>
     PD_INLINE void unpack_raw(bool clamp) {
-        if constexpr (sizeof(S) == 1) unpack(w, clamp);
+        if constexpr (sizeof(S) == 1) unpack(w, clamp, same_t<S, uint8_t>::value);
     }
     // D: float (the f32 stage feeding the register subtrees, latency variant), __half (an f16
     // stage: h[] stored as is) or int8
@@ -375,7 +391,8 @@ struct Chunk<PI8, CE> {
             uint32_t w[CE / 4];
 #pragma unroll
             for (int q = 0; q < CE / 4; ++q)
-                w[q] = __byte_perm(h2add(h[2 * q], 0x64806480u), h2add(h[2 * q + 1], 0x64806480u), 0x6420) ^ 0x80808080u;
+                w[q] = __byte_perm(h2add(h[2 * q], 0x64806480u), h2add(h[2 * q + 1], 0x64806480u), 0x6420) ^
+                       (same_t<D, uint8_t>::value ? 0u : 0x80808080u);
             vst<SP, CE, H>(p, w);
         }
     }
@@ -467,7 +484,8 @@ struct MemSrc {
     using V = typename P::v_t;
     const T* p;
     PD_INLINE V ld(T x) const {
-        if constexpr (!CHAN && sizeof(T) == 1) return __int_as_float(0x4B400000 + (int)x) - 12582912.0f;
+        if constexpr (same_t<T, uint8_t>::value) return __int_as_float(0x4B400000 + (int)x) - 12583040.0f;  // biased
+        else if constexpr (!CHAN && sizeof(T) == 1) return __int_as_float(0x4B400000 + (int)x) - 12582912.0f;
         else return P::ld(x);
     }
     PD_INLINE V v(int j) const { return ld(p[lane_id() + 32 * j]); }

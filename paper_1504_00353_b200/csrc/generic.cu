@@ -42,31 +42,34 @@ __global__ void __launch_bounds__(32) k_generic(const void* __restrict__ llr_, l
     const int NWK = (K + 31) / 32;
     uint32_t* const beta = (uint32_t*)(gsmem + g_align16((N > 1 ? N - 1 : 1) * (int)sizeof(S)));
     uint32_t* const stg = beta + NB;
-    const S* llr = (const S*)llr_;
+    using Ch = typename P::in_t;  // the channel (signed int8 or f32); stages are S (int8: biased bytes)
+    const Ch* llr = (const Ch*)llr_;
     const int l = lane_id();
     for (long long f = blockIdx.x; f < n_frames; f += gridDim.x) {
-        const S* chan = llr + f * N;
+        const Ch* chan = llr + f * N;
         for (int k = l; k < NB; k += 32) beta[k] = 0;
         __syncwarp();
         for (int pc = 0; pc < n_ops; ++pc) {
             const uint32_t w = __ldg(prog + pc);
             const int op = w & 15, n = 1 << ((w >> 4) & 31), off = (int)(w >> 9), h = n >> 1;
-            const S* src = n == N ? chan : st + (N - 2 * n);
+            const bool root = n == N;  // the root op reads the channel (uniform per op)
+            const S* srcs = root ? st : st + (N - 2 * n);
+            auto src_ld = [&](int i) -> V { return root ? P::ld(chan[i]) : P::ld(srcs[i]); };
             S* dst = st + (N - n);  // stage(n/2)
             switch (op) {
                 case OP_F:
-                    for (int i = l; i < h; i += 32) dst[i] = P::st(P::f(P::ld(src[i]), P::ld(src[i + h])));
+                    for (int i = l; i < h; i += 32) dst[i] = P::st(P::f(src_ld(i), src_ld(i + h)));
                     break;
                 case OP_G:
                     for (int i = l; i < h; i += 32)
-                        dst[i] = P::st(P::g(P::ld(src[i]), P::ld(src[i + h]), (beta[(off + i) >> 5] >> ((off + i) & 31)) & 1u));
+                        dst[i] = P::st(P::g(src_ld(i), src_ld(i + h), (beta[(off + i) >> 5] >> ((off + i) & 31)) & 1u));
                     break;
                 case OP_G0R:
-                    for (int i = l; i < h; i += 32) dst[i] = P::st(P::g0(P::ld(src[i]), P::ld(src[i + h])));
+                    for (int i = l; i < h; i += 32) dst[i] = P::st(P::g0(src_ld(i), src_ld(i + h)));
                     break;
                 case OP_R1:
                     for (int i0 = 0; i0 < n; i0 += 32) {
-                        const uint32_t b = __ballot_sync(FULL, i0 + l < n && P::hd(P::ld(src[i0 + l])));
+                        const uint32_t b = __ballot_sync(FULL, i0 + l < n && P::hd(src_ld(i0 + l)));
                         if (l == 0) {
                             if (n >= 32) beta[(off + i0) >> 5] = b;
                             else put_bits(beta, off, n, b);
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(32) k_generic(const void* __restrict__ llr_, l
                     bool neg;
                     if constexpr (P::kExactSum) {  // int8: exact, any order (reading C12)
                         typename P::acc_t t = 0;
-                        for (int i = l; i < n; i += 32) t = P::add(t, P::acc(P::ld(src[i])));
+                        for (int i = l; i < n; i += 32) t = P::add(t, P::acc(src_ld(i)));
 #pragma unroll
                         for (int o = 16; o; o >>= 1) t = P::add(t, __shfl_xor_sync(FULL, t, o));
                         neg = P::acc_neg(t);
@@ -86,10 +89,10 @@ __global__ void __launch_bounds__(32) k_generic(const void* __restrict__ llr_, l
                         typename P::acc_t t;
                         int start;
                         if (n <= 32) {
-                            t = P::acc(P::ld(src[l & (n - 1)]));
+                            t = P::acc(src_ld(l & (n - 1)));
                             start = h;
                         } else {
-                            for (int i = l; i < h; i += 32) dst[i] = P::add(P::ld(src[i]), P::ld(src[i + h]));
+                            for (int i = l; i < h; i += 32) dst[i] = P::add(src_ld(i), src_ld(i + h));
                             __syncwarp();
                             for (int m = h; m > 32; m >>= 1) {
                                 for (int i = l; i < m / 2; i += 32) dst[i] = P::add(dst[i], dst[i + m / 2]);
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(32) k_generic(const void* __restrict__ llr_, l
                     for (int i0 = 0; i0 < n; i0 += 32) {
                         const int i = i0 + l;
                         const bool in = i < n;
-                        const V x = in ? P::ld(src[i]) : V(0);
+                        const V x = in ? src_ld(i) : V(0);
                         const uint32_t b = __ballot_sync(FULL, in && P::hd(x));
                         par ^= __popc(b) & 1u;
                         if (l == 0) {
@@ -219,33 +222,36 @@ __global__ void __launch_bounds__(GB_T) k_generic_big(const void* __restrict__ l
     unsigned long long* const red = (unsigned long long*)(beta + NB);  // per-warp reduction slots
     uint32_t* const redp = (uint32_t*)(red + 32);
     S* const gst = (S*)gslot_all + (long long)blockIdx.x * generic_big_gslot<P>(N);
-    const S* llr = (const S*)llr_;
+    using Ch = typename P::in_t;  // the channel (signed int8 or f32); stages are S (int8: biased bytes)
+    const Ch* llr = (const Ch*)llr_;
     const int tid = threadIdx.x, l = lane_id(), wid = tid >> 5;
     // alpha of a node of size m (m < N): stage(m) at 2*GB - 2m in shared memory, else N - 2m globally
     auto stage = [&](int m) -> S* { return m <= GB_SMEM_MAX ? sst + (small - 2 * m) : gst + ((long long)N - 2LL * m); };
     for (long long f = blockIdx.x; f < n_frames; f += gridDim.x) {
-        const S* chan = llr + f * (long long)N;
+        const Ch* chan = llr + f * (long long)N;
         for (int k = tid; k < NB; k += GB_T) beta[k] = 0;
         __syncthreads();
         for (int pc = 0; pc < n_ops; ++pc) {
             const uint32_t w = __ldg(prog + pc);
             const int op = w & 15, n = 1 << ((w >> 4) & 31), off = (int)(w >> 9), h = n >> 1;
-            const S* src = n == N ? chan : stage(n);
+            const bool root = n == N;  // the root op reads the channel (uniform per op)
+            const S* srcs = root ? gst : stage(n);
+            auto src_ld = [&](int i) -> V { return root ? P::ld(chan[i]) : P::ld(srcs[i]); };
             S* dst = stage(h);
             switch (op) {
                 case OP_F:
-                    for (int i = tid; i < h; i += GB_T) dst[i] = P::st(P::f(P::ld(src[i]), P::ld(src[i + h])));
+                    for (int i = tid; i < h; i += GB_T) dst[i] = P::st(P::f(src_ld(i), src_ld(i + h)));
                     break;
                 case OP_G:
                     for (int i = tid; i < h; i += GB_T)
-                        dst[i] = P::st(P::g(P::ld(src[i]), P::ld(src[i + h]), (beta[(off + i) >> 5] >> ((off + i) & 31)) & 1u));
+                        dst[i] = P::st(P::g(src_ld(i), src_ld(i + h), (beta[(off + i) >> 5] >> ((off + i) & 31)) & 1u));
                     break;
                 case OP_G0R:
-                    for (int i = tid; i < h; i += GB_T) dst[i] = P::st(P::g0(P::ld(src[i]), P::ld(src[i + h])));
+                    for (int i = tid; i < h; i += GB_T) dst[i] = P::st(P::g0(src_ld(i), src_ld(i + h)));
                     break;
                 case OP_R1:
                     for (int i0 = 32 * wid; i0 < n; i0 += GB_T) {
-                        const uint32_t b = __ballot_sync(FULL, i0 + l < n && P::hd(P::ld(src[i0 + l])));
+                        const uint32_t b = __ballot_sync(FULL, i0 + l < n && P::hd(src_ld(i0 + l)));
                         if (l == 0) {
                             if (n >= 32) beta[(off + i0) >> 5] = b;
                             else put_bits(beta, off, n, b);
@@ -256,7 +262,7 @@ __global__ void __launch_bounds__(GB_T) k_generic_big(const void* __restrict__ l
                     bool neg;
                     if constexpr (P::kExactSum) {
                         typename P::acc_t t = 0;
-                        for (int i = tid; i < n; i += GB_T) t = P::add(t, P::acc(P::ld(src[i])));
+                        for (int i = tid; i < n; i += GB_T) t = P::add(t, P::acc(src_ld(i)));
 #pragma unroll
                         for (int o = 16; o; o >>= 1) t = P::add(t, __shfl_xor_sync(FULL, t, o));
                         if (l == 0) red[wid] = __float_as_uint(t);
@@ -268,10 +274,10 @@ __global__ void __launch_bounds__(GB_T) k_generic_big(const void* __restrict__ l
                     } else {
                         V t;
                         if (n <= 32) {
-                            t = P::ld(src[l & (n - 1)]);
+                            t = src_ld(l & (n - 1));
                             for (int o = h; o >= 1; o >>= 1) t = P::add(t, __shfl_xor_sync(FULL, t, o));
                         } else {
-                            for (int i = tid; i < h; i += GB_T) dst[i] = P::add(P::ld(src[i]), P::ld(src[i + h]));
+                            for (int i = tid; i < h; i += GB_T) dst[i] = P::add(src_ld(i), src_ld(i + h));
                             __syncthreads();
                             for (int m = h; m > 32; m >>= 1) {
                                 for (int i = tid; i < m / 2; i += GB_T) dst[i] = P::add(dst[i], dst[i + m / 2]);
@@ -295,7 +301,7 @@ __global__ void __launch_bounds__(GB_T) k_generic_big(const void* __restrict__ l
                     for (int i0 = 32 * wid; i0 < n; i0 += GB_T) {
                         const int i = i0 + l;
                         const bool in = i < n;
-                        const V x = in ? P::ld(src[i]) : V(0);
+                        const V x = in ? src_ld(i) : V(0);
                         const uint32_t b = __ballot_sync(FULL, in && P::hd(x));
                         par ^= __popc(b) & 1u;
                         if (l == 0) {
