@@ -304,6 +304,7 @@ void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::stri
     std::string m = e.warp(id, 0, "src");
     if (R >= 64) {
         o << "        wStoreBeta<" << R << ">(bw, beta + " << v.off / 32 << ");\n";
+        if (g_marks) o << "        " << g_marks->mark("StoreBeta<" + std::to_string(R) + ">") << "\n";
     } else {
         // R <= 32 only when the whole frame is this subtree (N <= 32): word 0.
         o << "        if (lane_id() == 0) beta[" << v.off / 32 << "] = " << m << ";\n";

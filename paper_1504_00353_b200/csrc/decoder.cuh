@@ -782,20 +782,29 @@ PD_INLINE void wComb0R(uint64_t& bw) {
 }
 
 // Write the beta of a finished warp subtree of size R >= 32 into the natural bit array:
-// word k (bits k*32 .. k*32+31 of the subtree) is the ballot of bw bit k.
+// word k (bits k*32 .. k*32+31 of the subtree) is the ballot of bw bit k.  The ballots are
+// warp-uniform, so every lane holds all NW words and lanes 0.. store them as 16-byte groups: two
+// instructions per word (predicate + vote) instead of seven (64-bit shift/compare, vote,
+// per-lane select), measured 658 -> ~150 cycles per 512-subtree on the batch-1 path.
 template <int R>
 PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
     static_assert(R >= 32 && R <= 2048, "");
     constexpr int NW = R / 32;
-    uint32_t keep[(NW + 31) / 32];
+    const uint32_t lo = (uint32_t)bw, hi = (uint32_t)(bw >> 32);
+    uint32_t wd[NW];
 #pragma unroll
-    for (int k = 0; k < NW; ++k) {
-        const uint32_t w = __ballot_sync(FULL, (uint32_t)(bw >> k) & 1u);
-        if (lane_id() == (unsigned)(k & 31)) keep[k >> 5] = w;
+    for (int k = 0; k < NW; ++k) wd[k] = __ballot_sync(FULL, ((k < 32 ? lo : hi) >> (k & 31)) & 1u);
+    // lane 0 stores them all (one predicate; a per-lane choice of group compiled to a jump table)
+    if (lane_id() == 0) {
+        if constexpr (NW >= 4) {
+#pragma unroll
+            for (int g = 0; g < NW / 4; ++g)
+                *reinterpret_cast<uint4*>(words + 4 * g) = make_uint4(wd[4 * g], wd[4 * g + 1], wd[4 * g + 2], wd[4 * g + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < NW; ++k) words[k] = wd[k];
+        }
     }
-#pragma unroll
-    for (int c = 0; c < (NW + 31) / 32; ++c)
-        if (lane_id() + 32 * c < (unsigned)NW) words[lane_id() + 32 * c] = keep[c];
 }
 
 // ------------------------------------------------------------------ CTA-scope operations
