@@ -75,6 +75,14 @@ template <class A>
 struct same_t<A, A> {
     static constexpr bool value = true;
 };
+template <bool B, class T, class F>
+struct cond_t {
+    using type = T;
+};
+template <class T, class F>
+struct cond_t<false, T, F> {
+    using type = F;
+};
 
 // POLAR_TRACE builds: clock64() after every op of the latency variant's critical path, block 0
 // thread 0 only, into the buffer the library passes (tools/trace_latency.py reads it back).
@@ -632,7 +640,10 @@ template <class P, int n, int s0, class Src>
 PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
     static_assert(n >= 64, "");
     constexpr int J = n / 32;
-    uint64_t hb = 0;
+    // the lane's J decision bits: 32-bit arithmetic up to n = 1024 (64-bit shifts cost two
+    // instructions each on the batch-1 critical path)
+    using HB = typename cond_t<(J <= 32), uint32_t, uint64_t>::type;
+    HB hb = 0;
     uint32_t idx;
     // balanced reductions (log2 J dependent steps instead of a J-long chain); the lowest index
     // among equal magnitudes still wins (C10): int8 packs the index into the key
@@ -641,7 +652,7 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const auto x = s.v(j);
-            hb |= (uint64_t)P::hd(x) << j;
+            hb |= (HB)P::hd(x) << j;
             kk[j] = P::mag_key(x) | (uint32_t)(j * 32 + lane_id());
         }
 #pragma unroll
@@ -654,7 +665,7 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const auto x = s.v(j);
-            hb |= (uint64_t)P::hd(x) << j;
+            hb |= (HB)P::hd(x) << j;
             kk[j] = P::mag_key(x);
             jj[j] = j;
         }
@@ -671,9 +682,9 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
         const uint32_t mn = __reduce_min_sync(FULL, kk[0]);
         idx = __reduce_min_sync(FULL, kk[0] == mn ? jj[0] * 32u + lane_id() : 0xffffffffu);
     }
-    const uint32_t parity = __popc(__ballot_sync(FULL, __popcll(hb) & 1)) & 1u;
-    if (parity && lane_id() == (idx & 31u)) hb ^= 1ull << (idx >> 5);
-    bw |= hb << s0;
+    const uint32_t parity = __popc(__ballot_sync(FULL, __popcll((uint64_t)hb) & 1)) & 1u;
+    if (parity && lane_id() == (idx & 31u)) hb ^= (HB)1 << (idx >> 5);
+    bw |= (uint64_t)hb << s0;
 }
 
 // RepSPC<n>: a node whose left child is a repetition code and right child an SPC
