@@ -832,7 +832,10 @@ PD_INLINE void wStoreBeta(uint64_t bw, uint32_t* words) {
 template <class P, int H, int T>
 __host__ __device__ constexpr int stage_unroll() {
     constexpr int step = chunk_elems<P, H, T>() * T;
-    constexpr int umax = T == 32 ? 4 : 1;  // the latency CTA (shared-memory stages, 128-register cap) needs none
+#ifndef POLAR_STAGE_U
+#define POLAR_STAGE_U 4
+#endif
+    constexpr int umax = T == 32 ? POLAR_STAGE_U : 1;  // the latency CTA (shared-memory stages, 128-register cap) needs none
     return H / step >= umax ? umax : H / step >= 2 ? 2 : 1;
 }
 template <class P, int T, int n, bool CLAMP, int SS, int DS, class S, class D>
