@@ -95,6 +95,7 @@ struct Emitter {
     int next_mask = 0;
     std::string ind = "        ";
     int body_root = -1;  // the node whose shared function body is being emitted
+    bool words = true;   // decisions as warp-uniform words (decoder.cuh BW<>), else one 64-bit word per lane
 
     std::string mask_name() { return "m" + std::to_string(next_mask++); }
     void mk(const std::string& label) {
@@ -165,10 +166,14 @@ struct Emitter {
             std::string args;
             for (int j = 0; j < (n >= 32 ? n / 32 : 1); ++j) args += (j ? ", " : "") + src_arr + "[" + std::to_string(j) + "]";
             const std::string m = mask_name();
-            o << ind << "const uint32_t " << m << " = " << fn << "<P>(" << args << ");\n";
+            o << ind << "const " << (n == 64 ? "uint64_t " : "uint32_t ") << m << " = " << fn << "<P>(" << args << ");\n";
             mk("shared<" + N_ + ">");
             if (n <= 32) return m;
-            o << ind << "bw |= (uint64_t)" << m << " << " << s0 << ";\n";
+            if (n != 64 || !words) {
+                std::cerr << "codegen: shared subtree functions above 32 values need decision words and size 64\n";
+                std::exit(3);
+            }
+            o << ind << "wSetWords64<" << s0 << ">(bw, " << m << ");\n";
             return "";
         }
         switch (v.kind) {
@@ -272,16 +277,17 @@ std::string Emitter::shared_fn(int id) {
     const int S = n >= 32 ? n / 32 : 1;
     for (int k = ilog2(n) - 1; k >= 0; --k)
         body << "    V r" << k << "[" << ((1 << k) >= 32 ? (1 << k) / 32 : 1) << "];\n";
-    body << "    uint64_t bw = 0;\n    (void)bw;\n";
+    body << "    BW<" << std::max(1, n / 32) << "> bw{};\n    (void)bw;\n";
     e.ind = "    ";
     std::string m = e.warp(id, 0, "RegSrc<P>{in}", "in");
     // the name is reserved only after the body: nested patterns get their definitions first
     sh->by_key[key] = fn;
-    sh->defs << "template <class P>\n__device__ __noinline__ uint32_t " << fn << "(";
+    sh->defs << "template <class P>\n__device__ __noinline__ " << (n == 64 ? "uint64_t " : "uint32_t ") << fn << "(";
     for (int j = 0; j < S; ++j) sh->defs << (j ? ", " : "") << "typename P::v_t a" << j;
     sh->defs << ") {\n    using V = typename P::v_t;\n    V in[" << S << "] = {";
     for (int j = 0; j < S; ++j) sh->defs << (j ? ", " : "") << "a" << j;
-    sh->defs << "};\n" << body.str() << "    return " << (n <= 32 ? m : std::string("(uint32_t)bw")) << ";\n}\n\n";
+    sh->defs << "};\n" << body.str() << "    return "
+             << (n <= 32 ? m : std::string("(uint64_t)bw.w[0] | ((uint64_t)bw.w[1] << 32)")) << ";\n}\n\n";
     return fn;
 }
 
@@ -299,8 +305,12 @@ void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::stri
         const int size = 1 << k;
         o << "        V r" << k << "[" << (size >= 32 ? size / 32 : 1) << "];\n";
     }
-    o << "        uint64_t bw = 0;\n        (void)bw;\n";
+    // decisions as warp-uniform words up to 512 values (16 registers), else one 64-bit word per lane
+    const bool words = R <= 512;
+    if (words) o << "        BW<" << std::max(1, R / 32) << "> bw{};\n        (void)bw;\n";
+    else o << "        uint64_t bw = 0;\n        (void)bw;\n";
     Emitter e{t, o, sh};
+    e.words = words;
     std::string m = e.warp(id, 0, "src");
     if (R >= 64) {
         o << "        wStoreBeta<" << R << ">(bw, beta + " << v.off / 32 << ");\n";

@@ -182,6 +182,8 @@ struct PF32 {
         return __fadd_rn(b, __uint_as_float(__float_as_uint(a) ^ (beta << 31)));
     }
     static PD_INLINE v_t g0(v_t a, v_t b) { return __fadd_rn(b, a); }
+    // g with beta given as the sign-bit mask (beta << 31)
+    static PD_INLINE v_t gs(v_t a, v_t b, uint32_t sgn) { return __fadd_rn(b, __uint_as_float(__float_as_uint(a) ^ sgn)); }
     static PD_INLINE bool hd(v_t a) { return a < 0.0f; }  // eq:info P:444-449, -0 -> 0 (C9)
     static PD_INLINE uint32_t mag_key(v_t a) { return __float_as_uint(a) & 0x7fffffffu; }
     static PD_INLINE acc_t acc(v_t a) { return a; }
@@ -214,6 +216,7 @@ struct PI8 {
     // saturating adder (max(-127) P:848): clamp(x) = copysign(min(|x|, 127), x)
     static PD_INLINE v_t g(v_t a, v_t b, uint32_t beta) { return fminxs(PF32::g(a, b, beta), 127.0f); }
     static PD_INLINE v_t g0(v_t a, v_t b) { return fminxs(__fadd_rn(b, a), 127.0f); }
+    static PD_INLINE v_t gs(v_t a, v_t b, uint32_t sgn) { return fminxs(PF32::gs(a, b, sgn), 127.0f); }
     static PD_INLINE bool hd(v_t a) { return a < 0.0f; }
     static PD_INLINE uint32_t mag_key(v_t a) { return __float_as_uint(a) & 0x7fffffffu; }
     static PD_INLINE acc_t acc(v_t a) { return a; }
@@ -685,6 +688,124 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
     const uint32_t parity = __popc(__ballot_sync(FULL, __popcll((uint64_t)hb) & 1)) & 1u;
     if (parity && lane_id() == (idx & 31u)) hb ^= (HB)1 << (idx >> 5);
     bw |= (uint64_t)hb << s0;
+}
+
+// ---------------------------------------------------- subtree decisions as warp-uniform words
+// BW<NW>: the decision bits of a warp subtree of 32*NW values as NW words, w[s] bit l =
+// beta[l + 32 s] -- the natural bit array itself, the same in every lane (ballots, XORs of
+// ballots).  The alternative (one 64-bit word per lane, bit s = beta[lane + 32 s]) needs a
+// transpose of ballots at the subtree's end and 64-bit shifts in every leaf and combine; here
+// a Rate-1 slot is one ballot, a combine one XOR per word, a replicated node's mask is stored as
+// is, and the store is lane 0 writing the words.  Used for subtrees up to 512 values (codegen).
+template <int NW>
+struct BW {
+    uint32_t w[NW];
+};
+// sign-bit mask of this lane's bit of word x (beta[lane + 32 s] << 31)
+PD_INLINE uint32_t lane_sgn(uint32_t x) { return (x << (31u - lane_id())) & 0x80000000u; }
+
+template <class P, int n, int s0, class Src, int NW>
+PD_INLINE void wG(const Src& s, typename P::v_t* c, const BW<NW>& bw, uint32_t ml) {
+    if constexpr (n >= 64) {
+#pragma unroll
+        for (int j = 0; j < n / 64; ++j) c[j] = P::gs(s.v(j), s.v(j + n / 64), lane_sgn(bw.w[s0 + j]));
+        PD_DUMPR(n, c);
+    } else {
+        wG<P, n, s0>(s, c, (uint64_t)0, ml);
+    }
+}
+template <class P, int n, int s0, class Src, int NW>
+PD_INLINE void wR1(const Src& s, BW<NW>& bw) {
+    static_assert(n >= 64, "");
+#pragma unroll
+    for (int j = 0; j < n / 32; ++j) bw.w[s0 + j] = __ballot_sync(FULL, P::hd(s.v(j)));
+}
+template <class P, int n, int s0, class Src, int NW>
+PD_INLINE void wRep(const Src& s, BW<NW>& bw) {
+    static_assert(n >= 64, "");
+    const uint32_t m = wRepDecide<P, n>(s) ? FULL : 0u;
+#pragma unroll
+    for (int j = 0; j < n / 32; ++j) bw.w[s0 + j] = m;
+}
+// SPC with the hard decisions as ballot words; the flip of the lowest-index least
+// reliable bit (C10) lands in the word idx / 32 by an unrolled select.
+template <class P, int n, int s0, class Src, int NW>
+PD_INLINE void wSPC(const Src& s, BW<NW>& bw) {
+    static_assert(n >= 64, "");
+    constexpr int J = n / 32;
+    uint32_t hw[J], par = 0, idx;
+    if constexpr (P::kPackedKey) {
+        uint32_t kk[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const auto x = s.v(j);
+            hw[j] = __ballot_sync(FULL, P::hd(x));
+            par ^= hw[j];
+            kk[j] = P::mag_key(x) | (uint32_t)(j * 32 + lane_id());
+        }
+#pragma unroll
+        for (int m = J; m > 1; m /= 2)
+#pragma unroll
+            for (int j = 0; j < m / 2; ++j) kk[j] = min(kk[j], kk[j + m / 2]);
+        idx = __reduce_min_sync(FULL, kk[0]) & 0xffffu;
+    } else {
+        uint32_t kk[J], jj[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const auto x = s.v(j);
+            hw[j] = __ballot_sync(FULL, P::hd(x));
+            par ^= hw[j];
+            kk[j] = P::mag_key(x);
+            jj[j] = j;
+        }
+#pragma unroll
+        for (int st = 1; st < J; st *= 2)
+#pragma unroll
+            for (int j = 0; j + st < J; j += 2 * st) {
+                const bool r = kk[j + st] < kk[j];
+                kk[j] = r ? kk[j + st] : kk[j];
+                jj[j] = r ? jj[j + st] : jj[j];
+            }
+        const uint32_t mn = __reduce_min_sync(FULL, kk[0]);
+        idx = __reduce_min_sync(FULL, kk[0] == mn ? jj[0] * 32u + lane_id() : 0xffffffffu);
+    }
+    const uint32_t flip = (__popc(par) & 1u) << (idx & 31u);
+#pragma unroll
+    for (int j = 0; j < J; ++j) bw.w[s0 + j] = hw[j] ^ ((idx >> 5) == (uint32_t)j ? flip : 0u);
+}
+template <int s, int NW>
+PD_INLINE void wDeposit(BW<NW>& bw, uint32_t m) {
+    bw.w[s] = m;
+}
+template <int n, int s0, int NW>
+PD_INLINE void wComb(BW<NW>& bw) {
+#pragma unroll
+    for (int k = 0; k < n / 64; ++k) bw.w[s0 + k] ^= bw.w[s0 + n / 64 + k];
+}
+template <int n, int s0, int NW>
+PD_INLINE void wComb0R(BW<NW>& bw) {
+#pragma unroll
+    for (int k = 0; k < n / 64; ++k) bw.w[s0 + k] |= bw.w[s0 + n / 64 + k];
+}
+template <int R, int NW>
+PD_INLINE void wStoreBeta(const BW<NW>& bw, uint32_t* words) {
+    static_assert(R / 32 == NW, "");
+    if (lane_id() == 0) {
+        if constexpr (NW >= 4) {
+#pragma unroll
+            for (int g = 0; g < NW / 4; ++g)
+                *reinterpret_cast<uint4*>(words + 4 * g) = make_uint4(bw.w[4 * g], bw.w[4 * g + 1], bw.w[4 * g + 2], bw.w[4 * g + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < NW; ++k) words[k] = bw.w[k];
+        }
+    }
+}
+// shared subtree functions of 64 values return their two words packed in 64 bits
+template <int s0, int NW>
+PD_INLINE void wSetWords64(BW<NW>& bw, uint64_t m) {
+    bw.w[s0] = (uint32_t)m;
+    bw.w[s0 + 1] = (uint32_t)(m >> 32);
 }
 
 // RepSPC<n>: a node whose left child is a repetition code and right child an SPC
