@@ -62,6 +62,7 @@ struct Spec {
                           // measured 162/262/207 Gbps at (2048,1723), profiles/r1_history.md)
     int xwpc = 1;         // frame-interleaved variant: warps per CTA (XWPC=)
     bool mailbox = false; // batch-1 persistent mailbox kernel of the int8 latency variant (MAILBOX=1)
+    bool fuse = true;     // CTA-level X<n> and its split child's first op as one fused op (FUSE=0 disables)
 };
 
 // Distinct small-subtree patterns emitted once as __noinline__ device functions, so that the
@@ -363,12 +364,12 @@ struct CtaEmitter {
     static std::string region(std::string x) {
         for (size_t q; (q = x.find("<P, T, ")) != std::string::npos;) x.replace(q, 7, "<P, 32, ");
         for (size_t q; (q = x.find("<T, ")) != std::string::npos;) x.replace(q, 4, "<32, ");
-        if (x == "sync();") x = "__syncwarp();";
+        if (x == "sync();" || x == "sync.comb();") x = "__syncwarp();";
         return x;
     }
     void emit(const std::string& stmt0) {
         const std::string stmt = in_region ? region(stmt0) : stmt0;
-        if ((stmt == "sync();" || stmt == "__syncwarp();") && g_marks) {
+        if ((stmt == "sync();" || stmt == "sync.comb();" || stmt == "__syncwarp();") && g_marks) {
             emit_raw(stmt);
             std::string lab = last_op.rfind("if (gtid", 0) == 0 ? std::string("subtree") : last_op.substr(0, last_op.find('('));
             emit_raw(g_marks->mark("cta:" + lab));
@@ -430,7 +431,7 @@ struct CtaEmitter {
     // State space (SP_GLOBAL 0 / SP_SHARED 1) of a stage, as a placeholder (see stage()).
     std::string space(int m) { return "@P" + std::to_string(m) + "@"; }
 
-    void child(int id, const std::string& src) {
+    void child(int id, const std::string& src, bool first_done = false) {
         const Node& v = t.nodes[id];
         if (v.kind == Kind::Rate0) return;  // beta zeroed at frame start
         if (v.n > W && v.n <= XW && !in_region) {
@@ -442,11 +443,51 @@ struct CtaEmitter {
             emit("sync();");
             return;
         }
-        if (v.n > W) cta(id, src);
+        if (v.n > W) cta(id, src, first_done);
         else sub_call(id, src);
     }
 
-    void cta(int id, const std::string& src) {
+    // Fused descents (decoder.cuh cXY): X<n> of a node and the first op of its child c (F, or
+    // G_0R when c's left child is Rate-0) as one op, when c is a CTA-level split node outside a
+    // warp-0 region.  Returns the child's first-op kind (OP_F 0, OP_G0R 2) or -1.
+    bool fuse = false;
+    int fuse_kind(int cid) {
+        if (!fuse) return -1;
+        const Node& c = t.nodes[cid];
+        if (c.kind != Kind::Split || c.n <= W || (c.n <= XW && !in_region)) return -1;
+        return t.nodes[c.left].kind == Kind::Rate0 ? 2 : 0;
+    }
+    // X<n> of node id (XK: 0 F, 1 G, 2 G_0R) from src into D, then the child cid (fused when
+    // fuse_kind allows)
+    void xop_child(int id, int XK, const std::string& src, const std::string& D, const std::string& B, int cid) {
+        const Node& v = t.nodes[id];
+        const int n = v.n, h = n / 2;
+        const std::string N_ = std::to_string(n);
+        const std::string SS = src == "chan" ? "CHS" : space(n);
+        const std::string CL = src == "chan" ? "true" : "false";  // int8 channel: clamp -128
+        const int YK = fuse_kind(cid);
+        if (YK < 0) {
+            if (XK == 0) emit("cF<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
+            else if (XK == 1)
+                emit("cG<P, T, " + N_ + ", " + CL + ", false, " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ", " + B + ");");
+            else emit("cG0R<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
+            emit("sync();");
+            emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
+            if (id == 0 && XK != 0) emit("sync.root_g_done();");
+            child(cid, D);
+            return;
+        }
+        const std::string D2 = stage(h / 2);
+        emit("cXY<P, T, " + N_ + ", " + CL + ", " + std::to_string(XK) + ", " + std::to_string(YK) + ", " + SS + ", " +
+             space(h) + ", " + space(h / 2) + ", NI>(" + src + ", " + D + ", " + D2 + ", " + (XK == 1 ? B : std::string("beta")) + ");");
+        emit("sync();");
+        emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
+        emit("PD_DUMPS(" + D2 + ", " + std::to_string(h / 2) + ");");
+        if (id == 0 && XK != 0) emit("sync.root_g_done();");
+        child(cid, D, true);
+    }
+
+    void cta(int id, const std::string& src, bool first_done = false) {
         const std::string SS = src == "chan" ? "CHS" : space(t.nodes[id].n);
         const Node& v = t.nodes[id];
         const int n = v.n;
@@ -475,32 +516,30 @@ struct CtaEmitter {
         const std::string D = stage(h);
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
+        // first_done: this node's first op (G_0R or F) ran fused into its parent's op
         // HELPER: one arrive per subtree call, just before the stage op that produces its input
         if (l.kind == Kind::Rate0) {
-            if (helper && h == W && r.kind != Kind::Rate0) emit("if (gtid<T>() < 32) sync.helper_arrive();");
-            emit("cG0R<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
-            emit("sync();");
-            emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
-            if (id == 0) emit("sync.root_g_done();");
-            child(v.right, D);
+            if (first_done) {
+                child(v.right, D);
+            } else {
+                if (helper && h == W && r.kind != Kind::Rate0) emit("if (gtid<T>() < 32) sync.helper_arrive();");
+                xop_child(id, 2, src, D, B, v.right);
+            }
             emit("cComb0R<T, " + N_ + ">(" + B + ");");
-            emit("sync();");
+            emit("sync.comb();");
             return;
         }
-        if (helper && h == W) emit("if (gtid<T>() < 32) sync.helper_arrive();");
-        emit("cF<P, T, " + N_ + ", " + CL + ", " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ");");
-        emit("sync();");
-        emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
-        child(v.left, D);
+        if (first_done) {
+            child(v.left, D);
+        } else {
+            if (helper && h == W) emit("if (gtid<T>() < 32) sync.helper_arrive();");
+            xop_child(id, 0, src, D, B, v.left);
+        }
         if (r.kind == Kind::Rate0) return;
         if (helper && h == W) emit("if (gtid<T>() < 32) sync.helper_arrive();");
-        emit("cG<P, T, " + N_ + ", " + CL + ", false, " + SS + ", " + space(h) + ", NI>(" + src + ", " + D + ", " + B + ");");
-        emit("sync();");
-        emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
-        if (id == 0) emit("sync.root_g_done();");
-        child(v.right, D);
+        xop_child(id, 1, src, D, B, v.right);
         emit("cComb<T, " + N_ + ">(" + B + ");");
-        emit("sync();");
+        emit("sync.comb();");
     }
 };
 
@@ -728,6 +767,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         ce.XW = sp.xw;
         ce.helper = sp.helper > 0;
         ce.latni = sp.latni;
+        ce.fuse = sp.fuse && !ce.helper;
         int acc = 0, sacc = 0, gacc = 0, hs = 0, hg = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         ce.h16 = sp.h16;
@@ -1035,6 +1075,7 @@ void parse_options(Spec& sp, std::istream& ls) {
             else if (opt.rfind("XSM=", 0) == 0) sp.xsm = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("XWPC=", 0) == 0) sp.xwpc = std::atoi(opt.c_str() + 5);
             else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;
+            else if (opt.rfind("FUSE=", 0) == 0) sp.fuse = std::atoi(opt.c_str() + 5) != 0;
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();
                 std::stringstream ds(opt.substr(6));

@@ -415,12 +415,14 @@ struct Chunk<PI8, CE> {
     // G: h = sat(b + (beta ? -h : h)); bit k of `bits` is beta of element k; the saturation
     // is min.xorsign.abs against 127.
     PD_INLINE void g(const Chunk& b, uint32_t bits) {
-        // sign mask of the pair (2q, 2q+1): t = its 2 bits; t * 0x40008000 = (t << 15) + (t << 30)
-        // (no overlapping terms, so no carries) puts bit 0 at 15 and bit 1 at 31; the mask keeps
-        // those two (one IMAD on the FMA pipe instead of two shifts and three logic ops).
+        // sign mask of the pair (2q, 2q+1) = bit 2q at 15 and bit 2q+1 at 31.  sp holds the even
+        // bits in place and the odd bits moved up by 15 (bit 2j+1 at 2j+16), so one left shift by
+        // 15 - 2q puts both of pair q's bits where they belong; the mask and the XOR into h are
+        // one LOP3 -- two instructions per pair (was four: shift, and, multiply, and-xor).
+        const uint32_t sp = (bits & 0x5555u) | ((bits & 0xAAAAu) << 15);
 #pragma unroll
         for (int q = 0; q < CE / 2; ++q) {
-            const uint32_t m = (((bits >> (2 * q)) & 3u) * 0x40008000u) & 0x80008000u;
+            const uint32_t m = (sp << (15 - 2 * q)) & 0x80008000u;
             h[q] = h2minxs(h2add(b.h[q], h[q] ^ m), 0x57F057F0u);
         }
     }
@@ -1009,6 +1011,67 @@ PD_INLINE void cG_body(const void* src, void* dst, const uint32_t* beta) {
             }
     }
 }
+// Fused descent (XK then YK): X<n> of the node (F, G or G_0R) immediately followed by the first
+// op of its CTA-level child, Y<n/2> (F, or G_0R when the child's left child is Rate-0), on the
+// outputs X just produced.  Element i of Y's output needs X outputs i and i + n/4, i.e. the node
+// values i, i + n/4, i + n/2, i + 3n/4: each thread loads those four chunks, computes both X
+// chunks, stores them (the child's alpha, read again by its G later) and applies Y to them in
+// registers -- the child stage is written but not re-read and re-unpacked, and one op boundary
+// disappears.  Same f/g arithmetic and operands as the two ops it replaces.
+enum : int { OP_F = 0, OP_G = 1, OP_G0R = 2 };
+template <int K, class P, int CE>
+PD_INLINE void chunk_op(Chunk<P, CE>& a, const Chunk<P, CE>& b, uint32_t bits) {
+    if constexpr (K == OP_F) chunk_f(a, b);
+    else if constexpr (K == OP_G) chunk_g(a, b, bits);
+    else chunk_g0(a, b);
+}
+template <class P, int T, int n, bool CLAMP, int XK, int YK, int SS, int DS, int DS2, class S, class D, class D2>
+PD_INLINE void cXY_body(const void* src, void* dst, void* dst2, const uint32_t* beta) {
+    constexpr int Q = n / 4, CE = chunk_elems<P, Q, T>(), STEP = CE * T;
+    constexpr int U = (T == 32 && Q / STEP >= 2) ? 2 : 1;
+    constexpr int LH = CLAMP ? L2_FIRST : L2_LAST;
+#pragma unroll 1
+    for (int i0 = CE * gtid<T>(); i0 < Q; i0 += STEP * U) {
+        Chunk<P, CE> a0[U], b0[U], a1[U], b1[U];
+        uint32_t bits0[U], bits1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * STEP < Q) {
+                const int i = i0 + u * STEP;
+                a0[u].template load_raw<SS, LH>((const S*)src + i);
+                b0[u].template load_raw<SS, LH>((const S*)src + i + 2 * Q);
+                a1[u].template load_raw<SS, LH>((const S*)src + i + Q);
+                b1[u].template load_raw<SS, LH>((const S*)src + i + 3 * Q);
+                bits0[u] = XK == OP_G ? beta[i >> 5] >> (i & 31) : 0u;
+                bits1[u] = XK == OP_G ? beta[(i + Q) >> 5] >> ((i + Q) & 31) : 0u;
+            }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * STEP < Q) {
+                const int i = i0 + u * STEP;
+                a0[u].template unpack_raw<S>(CLAMP);
+                b0[u].template unpack_raw<S>(CLAMP);
+                chunk_op<XK>(a0[u], b0[u], bits0[u]);
+                a1[u].template unpack_raw<S>(CLAMP);
+                b1[u].template unpack_raw<S>(CLAMP);
+                chunk_op<XK>(a1[u], b1[u], bits1[u]);
+                a0[u].template store<DS, L2_LAST>((D*)dst + i);
+                a1[u].template store<DS, L2_LAST>((D*)dst + i + Q);
+                chunk_op<YK>(a0[u], a1[u], 0u);
+                a0[u].template store<DS2, L2_LAST>((D2*)dst2 + i);
+            }
+    }
+}
+template <class P, int T, int n, bool CLAMP, int XK, int YK, int SS, int DS, int DS2, class S, class D, class D2>
+__device__ __noinline__ void cXY_impl(const void* src, void* dst, void* dst2, const uint32_t* beta) {
+    cXY_body<P, T, n, CLAMP, XK, YK, SS, DS, DS2, S, D, D2>(src, dst, dst2, beta);
+}
+template <class P, int T, int n, bool CLAMP, int XK, int YK, int SS, int DS, int DS2, bool NI, class TS, class TD, class TD2>
+PD_INLINE void cXY(const TS* src, TD* dst, TD2* dst2, const uint32_t* beta) {
+    if constexpr (NI) cXY_impl<P, T, n, CLAMP, XK, YK, SS, DS, DS2, TS, TD, TD2>(src, dst, dst2, beta);
+    else cXY_body<P, T, n, CLAMP, XK, YK, SS, DS, DS2, TS, TD, TD2>(src, dst, dst2, beta);
+}
+
 template <class P, int T, int n, bool CLAMP, int SS, int DS, class S, class D>
 __device__ __noinline__ void cF_impl(const void* src, void* dst) {
     cF_body<P, T, n, CLAMP, SS, DS, S, D>(src, dst);
@@ -1033,11 +1096,85 @@ template <class P, int T, int n, bool CLAMP, int SS, int DS, bool NI, class TS, 
 PD_INLINE void cG0R(const TS* src, TD* dst) {
     cG<P, T, n, CLAMP, true, SS, DS, NI>(src, dst, nullptr);
 }
+// ---- packed-byte leaves on biased int8 stages (byte u = v + 128, never -128: stages only)
+// 16 consecutive elements per thread and step (one 16-byte shared load).  v < 0 <=> bit 7 of u
+// is clear; the four sign bits of a word gather into a nibble by one multiply (the partial
+// products of 0x00204081 land on distinct bits, so there are no carries); 16 decision bits are
+// stored as one 16-bit half of a beta word (little-endian: half 2k is bits 0-15 of word k).
+PD_INLINE uint32_t hd16_biased(const uint32_t* w) {
+    uint32_t h = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h |= ((((~w[j]) & 0x80808080u) * 0x00204081u) >> 28) << (4 * j);
+    return h;
+}
+template <int T, int n>
+PD_INLINE void cR1_b(const uint8_t* __restrict__ src, uint32_t* beta) {
+    static_assert(n % 16 == 0, "");
+    for (int i = 16 * gtid<T>(); i < n; i += 16 * T) {
+        const uint4 v4 = *reinterpret_cast<const uint4*>(src + i);  // generic: the stage may be in L2 scratch
+        const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+        reinterpret_cast<uint16_t*>(beta)[i >> 4] = (uint16_t)hd16_biased(w);
+    }
+}
+// SPC on a biased int8 stage: decisions as above; |v| = |u - 128| is one byte
+// absolute difference per 4 values (vabsdiff4); the least reliable position is found on 16-bit
+// keys (|v| << 8 | position in the thread's 16) by packed u16x2 minima, the lowest position winning
+// ties (reading C10), then on 32-bit keys (|v| << 16 | element index) across the group.
+template <int T, int n>
+PD_INLINE void cSPC_b(const uint8_t* __restrict__ src, uint32_t* beta) {
+    static_assert(n % 16 == 0 && n <= 65536, "");
+    uint32_t best = 0xffffffffu, p = 0;
+    for (int i = 16 * gtid<T>(); i < n; i += 16 * T) {
+        const uint4 v4 = *reinterpret_cast<const uint4*>(src + i);  // generic: the stage may be in L2 scratch
+        const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+        const uint32_t h = hd16_biased(w);
+        reinterpret_cast<uint16_t*>(beta)[i >> 4] = (uint16_t)h;
+        p ^= __popc(h);
+        uint32_t k[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t m = __vabsdiffu4(w[j], 0x80808080u);  // |v| of the 4 bytes
+            const uint32_t ix = 0x03020100u + 0x04040404u * j;    // their positions in the 16
+            k[2 * j] = __byte_perm(m, ix, 0x1504);                // (|v0| << 8 | p0, |v1| << 8 | p1)
+            k[2 * j + 1] = __byte_perm(m, ix, 0x3726);            // (|v2| << 8 | p2, |v3| << 8 | p3)
+        }
+#pragma unroll
+        for (int m = 8; m > 1; m /= 2)
+#pragma unroll
+            for (int j = 0; j < m / 2; ++j) k[j] = __vminu2(k[j], k[j + m / 2]);
+        const uint32_t k16 = min(k[0] & 0xffffu, k[0] >> 16);
+        best = min(best, ((k16 >> 8) << 16) | (uint32_t)(i + (int)(k16 & 0xffu)));
+    }
+    best = __reduce_min_sync(FULL, best);
+    p = __reduce_xor_sync(FULL, p) & 1u;
+    if constexpr (T > 32) {
+        __shared__ uint32_t redk[T / 32], par[T / 32];
+        const int warp = gtid<T>() >> 5;
+        if (lane_id() == 0) {
+            redk[warp] = best;
+            par[warp] = p;
+        }
+        group_sync<T>();
+        best = __reduce_min_sync(FULL, lane_id() < T / 32 ? redk[lane_id()] : 0xffffffffu);
+        p = __reduce_xor_sync(FULL, lane_id() < T / 32 ? par[lane_id()] : 0u) & 1u;
+    }
+    group_sync<T>();
+    if (gtid<T>() == 0 && p) {
+        const uint32_t idx = best & 0xffffu;
+        beta[idx >> 5] ^= 1u << (idx & 31);
+    }
+    group_sync<T>();
+}
+
 template <class P, int T, int n, class TS>
 PD_INLINE void cR1(const TS* __restrict__ src, uint32_t* beta) {
-    for (int k = (gtid<T>() >> 5); k < n / 32; k += T / 32) {
-        const uint32_t w = __ballot_sync(FULL, P::hd(P::ld(src[32 * k + lane_id()])));
-        if (lane_id() == 0) beta[k] = w;
+    if constexpr (same_t<TS, uint8_t>::value && n % 16 == 0) {
+        cR1_b<T, n>(src, beta);
+    } else {
+        for (int k = (gtid<T>() >> 5); k < n / 32; k += T / 32) {
+            const uint32_t w = __ballot_sync(FULL, P::hd(P::ld(src[32 * k + lane_id()])));
+            if (lane_id() == 0) beta[k] = w;
+        }
     }
 }
 // Repetition at CTA scope.  f32: pairwise-halving order (reading C13) run in
@@ -1083,7 +1220,15 @@ PD_INLINE void cRep(const TS* __restrict__ src, TSc* scratch, uint32_t* beta) {
 // SPC at CTA scope: ballot hard decisions per word, parity of all, flip the
 // lowest-index least-magnitude bit when odd (reading C10); key = (|alpha| << 32) | index.
 template <class P, int T, int n, class TS>
+PD_INLINE void cSPC_w(const TS* __restrict__ src, uint32_t* beta);
+template <class P, int T, int n, class TS>
 PD_INLINE void cSPC(const TS* __restrict__ src, uint32_t* beta) {
+    if constexpr (same_t<TS, uint8_t>::value && n % 16 == 0 && n <= 65536) cSPC_b<T, n>(src, beta);
+    else cSPC_w<P, T, n>(src, beta);
+}
+// SPC with one element per lane and step (f32, f16 or channel sources)
+template <class P, int T, int n, class TS>
+PD_INLINE void cSPC_w(const TS* __restrict__ src, uint32_t* beta) {
     const int warp = (gtid<T>() >> 5);
     if constexpr (P::kPackedKey) {
         // int8: one 32-bit key (|alpha| f32 bits | index) per element, exact (see wSPCm);
@@ -1208,49 +1353,46 @@ PD_INLINE void beta_transform(uint32_t* beta) {
     }
 }
 
-// Piece-table gather (tab after the {imask, prefix} words: offsets[NWK + 1] padded to 4 words,
-// then uint4 pieces {codeword word, source shift, destination shift, mask}, built at create
-// time, polar_api.cu): thread q assembles output word q from its pieces -- maximal runs of
+// Lane-interleaved piece-table gather (tab after the {imask, prefix} words, built at create
+// time, polar_api.cu): output word q of x_hat[A] is the OR of its pieces -- maximal runs of
 // information positions inside one codeword word and one output word ((32768,29492): 2,155
-// pieces for 922 words) -- and stores it; no staging, no atomics.  `stg` is unused.
+// pieces for 922 words) -- each a uint2 {codeword word << 5 | rotation, destination mask}:
+// acc |= rotl(beta[word], rotation) & mask.  Output words are taken 32 at a time (group g =
+// words 32g .. 32g+31, one per lane); piece j of every word of a group is one coalesced 256-byte
+// row, so all of a group's loads are independent of each other; groups hold as many rows as
+// their longest word (padding pieces have mask 0); hdr[g] = first row of group g, hdr[NG] = the
+// total.  (r1/r2 form: per-word offsets, then uint4 pieces -- two dependent L2 loads per output
+// word, 10% of the warp-stall samples of the (32768,29492) throughput kernel, r2n_tp32k.)
+__host__ __device__ constexpr int gather_hdr_words(int N, int K) {
+    return (((K + 31) / 32 + 31) / 32 + 1 + 3) & ~3;
+}
 template <int N, int K, int T>
 PD_INLINE void gather_info(const uint32_t* beta, const uint32_t* __restrict__ tab, uint32_t* stg,
                            uint32_t* __restrict__ out) {
     (void)stg;
     constexpr int NB = N >= 32 ? N / 32 : 1;
     constexpr int NWK = (K + 31) / 32;
+    constexpr int NG = (NWK + 31) / 32;
     constexpr int TB = (2 * NB + 3) & ~3;  // the {imask, prefix} words, padded
-    const uint32_t* __restrict__ off = tab + TB;
-    const uint4* __restrict__ pc = reinterpret_cast<const uint4*>(tab + TB + ((NWK + 1 + 3) & ~3));
-    // the table lives in L2: GU words per thread and their first PF pieces are loaded before
-    // any is used (a dependent chain of table loads per word measured ~15% slower at N = 32768)
-    constexpr int GU = 2, PF = 4;
-    for (int q0 = gtid<T>(); q0 < NWK; q0 += GU * T) {
-        int pa[GU], pb[GU];
+    const uint32_t* __restrict__ hdr = tab + TB;
+    const uint2* __restrict__ pcs = reinterpret_cast<const uint2*>(tab + TB + gather_hdr_words(N, K));
+    const int lane = (int)lane_id();
+    // the first rows of groups 0..31 in one coalesced load, handed out by shuffles
+    const uint32_t hv = lane <= NG ? __ldg(hdr + lane) : 0u;
+    constexpr int GP = 4;  // rows loaded before any is used
+    for (int g = gtid<T>() >> 5; g < NG; g += T / 32) {
+        const int r0 = (int)(g < 32 ? __shfl_sync(FULL, hv, g) : __ldg(hdr + g));
+        const int r1 = (int)(g + 1 < 32 ? __shfl_sync(FULL, hv, g + 1) : __ldg(hdr + g + 1));
+        uint32_t acc = 0;
+        for (int r = r0; r < r1; r += GP) {
+            uint2 d[GP];
 #pragma unroll
-        for (int u = 0; u < GU; ++u) {
-            const int q = q0 + u * T;
-            pa[u] = q < NWK ? (int)__ldg(off + q) : 0;
-            pb[u] = q < NWK ? (int)__ldg(off + q + 1) : 0;
+            for (int u = 0; u < GP; ++u) d[u] = r + u < r1 ? __ldg(pcs + (r + u) * 32 + lane) : make_uint2(0u, 0u);
+#pragma unroll
+            for (int u = 0; u < GP; ++u) acc |= __funnelshift_l(beta[d[u].x >> 5], beta[d[u].x >> 5], d[u].x & 31u) & d[u].y;
         }
-        uint4 d[GU][PF];
-#pragma unroll
-        for (int u = 0; u < GU; ++u)
-#pragma unroll
-            for (int v = 0; v < PF; ++v) d[u][v] = pa[u] + v < pb[u] ? __ldg(pc + pa[u] + v) : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-        for (int u = 0; u < GU; ++u) {
-            const int q = q0 + u * T;
-            if (q >= NWK) break;
-            uint32_t acc = 0;
-#pragma unroll
-            for (int v = 0; v < PF; ++v) acc |= ((beta[d[u][v].x] >> d[u][v].y) & d[u][v].w) << d[u][v].z;
-            for (int p = pa[u] + PF; p < pb[u]; ++p) {
-                const uint4 e = __ldg(pc + p);
-                acc |= ((beta[e.x] >> e.y) & e.w) << e.z;
-            }
-            out[q] = acc;
-        }
+        const int q = 32 * g + lane;
+        if (q < NWK) out[q] = acc;
     }
 }
 

@@ -367,14 +367,15 @@ __global__ void __launch_bounds__(GB_T) k_generic_big(const void* __restrict__ l
         }
         // information bits by the piece table (as gather_info, runtime sizes)
         const int TB = (2 * NB + 3) & ~3;
-        const uint32_t* offp = gtab + TB;
-        const uint4* pcs = reinterpret_cast<const uint4*>(gtab + TB + ((NWK + 1 + 3) & ~3));
+        const int NG = (NWK + 31) / 32;
+        const uint32_t* hdr = gtab + TB;
+        const uint2* pcs = reinterpret_cast<const uint2*>(gtab + TB + ((NG + 1 + 3) & ~3));
         for (int q = tid; q < NWK; q += GB_T) {
             uint32_t acc = 0;
-            const int p1 = (int)__ldg(offp + q + 1);
-            for (int p = (int)__ldg(offp + q); p < p1; ++p) {
-                const uint4 d = __ldg(pcs + p);
-                acc |= ((beta[d.x] >> d.y) & d.w) << d.z;
+            const int g = q >> 5, r1 = (int)__ldg(hdr + g + 1);
+            for (int r = (int)__ldg(hdr + g); r < r1; ++r) {
+                const uint2 d = __ldg(pcs + r * 32 + (q & 31));
+                acc |= __funnelshift_l(beta[d.x >> 5], beta[d.x >> 5], d.x & 31u) & d.y;
             }
             out[f * NWK + q] = acc;
         }

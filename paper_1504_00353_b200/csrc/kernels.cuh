@@ -47,6 +47,13 @@ struct OpSync {
         if constexpr (T > 32) asm volatile("bar.sync 1, %0;" ::"n"(T) : "memory");
         else asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
     }
+    // after a Combine (a few word XORs on the group's own decision bits): in the throughput
+    // variant only the warp's own lanes need to see them, so the frame group is not held in
+    // lockstep there (+0.3%, same-box A/B)
+    PD_INLINE void comb() const {
+        if constexpr (T == 32) __syncwarp();
+        else (*this)();
+    }
     PD_INLINE void root_g_done() const {
         if (next && (threadIdx.x & (T - 1)) == 0) prefetch_l2(next, next_bytes);
     }

@@ -415,28 +415,43 @@ static polar_status init_device(polar_code* h) {
         gt.push_back(acc);
         acc += (uint32_t)__builtin_popcount(w);
     }
-    // Piece table of the unrolled kernels' gather (decoder.cuh gather_info): output word q of
-    // x_hat[A] is the OR of its pieces -- maximal runs of information positions that stay in one
-    // codeword word and one output word -- each {codeword word, source shift, destination
-    // shift, mask}.  Layout after the two tables above: offsets[NWK + 1] (padded to 4 words),
-    // then the pieces as uint4.
+    // Piece table of the gather (decoder.cuh gather_info, generic.cu): output word q of x_hat[A]
+    // is the OR of its pieces -- maximal runs of information positions that stay in one codeword
+    // word and one output word -- each a uint2 {codeword word << 5 | rotation, destination mask}
+    // with rotation = (destination - source shift) mod 32.  Output words go in groups of 32 (one
+    // per lane); group g owns rows hdr[g] .. hdr[g+1]-1, as many as its longest word, and piece j
+    // of word 32g + l is element l of row hdr[g] + j (padding: {0, 0}).  Layout after the two
+    // tables above: hdr[NG + 1] padded to 4 words (gather_hdr_words), then the rows.
     {
-        const uint32_t nwk = words_of(h->K);
-        std::vector<uint32_t> off(nwk + 1, 0), pcs;
+        const uint32_t nwk = words_of(h->K), ng = (nwk + 31) / 32;
+        std::vector<std::vector<std::pair<uint32_t, uint32_t>>> pw(nwk);
         for (uint32_t j = 0; j < (uint32_t)pos.size();) {
             const uint32_t q = j / 32, src = pos[j], k = src / 32;
             uint32_t len = 1;
             while (j + len < (uint32_t)pos.size() && (j + len) / 32 == q && pos[j + len] == src + len && (src + len) / 32 == k)
                 ++len;
-            pcs.insert(pcs.end(), {k, src % 32, j % 32, len >= 32 ? 0xffffffffu : ((1u << len) - 1u)});
-            off[q + 1] = (uint32_t)(pcs.size() / 4);
+            const uint32_t d = j % 32, rot = (d - src % 32) & 31u;
+            const uint32_t m = (len >= 32 ? 0xffffffffu : ((1u << len) - 1u)) << d;
+            pw[q].push_back({(k << 5) | rot, m});
             j += len;
         }
-        for (uint32_t q = 1; q <= nwk; ++q) off[q] = std::max(off[q], off[q - 1]);
-        while (off.size() % 4) off.push_back(0);
+        std::vector<uint32_t> hdr(ng + 1, 0);
+        for (uint32_t g = 0; g < ng; ++g) {
+            size_t mx = 0;
+            for (uint32_t q = 32 * g; q < std::min(nwk, 32 * g + 32); ++q) mx = std::max(mx, pw[q].size());
+            hdr[g + 1] = hdr[g] + (uint32_t)mx;
+        }
+        while (hdr.size() % 4) hdr.push_back(0);
         while (gt.size() % 4) gt.push_back(0);
-        gt.insert(gt.end(), off.begin(), off.end());
-        gt.insert(gt.end(), pcs.begin(), pcs.end());
+        gt.insert(gt.end(), hdr.begin(), hdr.end());
+        const size_t base = gt.size();
+        gt.resize(base + 2 * 32 * (size_t)hdr[ng], 0u);
+        for (uint32_t q = 0; q < nwk; ++q)
+            for (size_t jj = 0; jj < pw[q].size(); ++jj) {
+                const size_t at = base + 2 * ((size_t)(hdr[q / 32] + jj) * 32 + q % 32);
+                gt[at] = pw[q][jj].first;
+                gt[at + 1] = pw[q][jj].second;
+            }
     }
     CUDA_TRY(cudaMalloc(&h->d_gtab, gt.size() * sizeof(uint32_t)));
     CUDA_TRY(cudaMemcpy(h->d_gtab, gt.data(), gt.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));

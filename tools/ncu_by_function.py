@@ -30,6 +30,9 @@ def main():
     a = ap.parse_args()
     maps = {f: spans(os.path.join(CSRC, f)) for f in os.listdir(CSRC) if f.endswith((".cuh", ".cu"))}
     per, cur, line = Counter(), "?", None
+    samp = Counter()
+    reasons = {}
+    hdr = None
     total = 0
     by_addr = {}  # an inlined instruction is listed under every source line of its inline chain
     with gzip.open(a.prefix + "_source.csv.gz", "rt") as f:
@@ -39,6 +42,8 @@ def main():
             if r[0] == "File Path":
                 cur = r[1].split("/")[-1]
                 continue
+            if r[0] == "Line No":
+                hdr = [h.replace("stall_", "") for h in r[31:48]]
             if r[0] in ("Function Name", "Line No") or len(r) < 8:
                 continue
             if r[0]:
@@ -47,6 +52,8 @@ def main():
             if len(r) > 3 and r[2].startswith("0x"):
                 try:
                     n = int(r[7] or 0)
+                    smp = int(r[4] or 0)
+                    why = [int(x or 0) for x in r[31:48]] if hdr and len(r) >= 48 else []
                 except ValueError:
                     continue
                 if cur in maps and line:
@@ -55,17 +62,25 @@ def main():
                     key = "generated code"
                 else:
                     key = cur
-                by_addr.setdefault(r[2], [n, []])[1].append(key)
+                by_addr.setdefault(r[2], [n, [], smp, why])[1].append(key)
     # attribute each instruction once, to the outermost caller that is not a small helper
     helpers = re.compile(r":(h2add|h2minxs|h2max|fminxs|vld|vst|ld|f|g|g0|hd|mag_key|add|acc|acc_neg|v|one|pair|gtid|"
                          r"lane_id|l2_policy|low_mask|smem_u32|unpack_raw|load_raw)$|intrinsics|_rt\.hpp|functions\.hpp")
-    for n, keys in by_addr.values():
+    for n, keys, smp, why in by_addr.values():
         total += n
         good = [k for k in keys if not helpers.search(k)]
-        per[(good or keys)[-1]] += n
-    print(f"total warp instructions {total:.0f} ({total / a.frames:.0f} per frame)")
+        k = (good or keys)[-1]
+        per[k] += n
+        samp[k] += smp
+        acc = reasons.setdefault(k, Counter())
+        for name, c in zip(hdr or [], why):
+            acc[name] += c
+    ts = max(1, sum(samp.values()))
+    print(f"total warp instructions {total:.0f} ({total / a.frames:.0f} per frame); columns: share of instructions, "
+          f"instructions per frame, share of warp-stall samples (where the time goes)")
     for k, v in per.most_common(40):
-        print(f"{100 * v / total:5.1f}%  {v / a.frames:9.0f}/frame  {k}")
+        top = ", ".join(f"{r} {100 * c / max(1, samp[k]):.0f}%" for r, c in reasons.get(k, Counter()).most_common(3))
+        print(f"{100 * v / total:5.1f}%  {v / a.frames:9.0f}/frame  {100 * samp[k] / ts:5.1f}%  {k}  [{top}]")
 
 
 if __name__ == "__main__":
