@@ -1355,16 +1355,22 @@ PD_INLINE void beta_transform(uint32_t* beta) {
 
 // Lane-interleaved piece-table gather (tab after the {imask, prefix} words, built at create
 // time, polar_api.cu): output word q of x_hat[A] is the OR of its pieces -- maximal runs of
-// information positions inside one codeword word and one output word ((32768,29492): 2,155
-// pieces for 922 words) -- each a uint2 {codeword word << 5 | rotation, destination mask}:
-// acc |= rotl(beta[word], rotation) & mask.  Output words are taken 32 at a time (group g =
-// words 32g .. 32g+31, one per lane); piece j of every word of a group is one coalesced 256-byte
-// row, so all of a group's loads are independent of each other; groups hold as many rows as
-// their longest word (padding pieces have mask 0); hdr[g] = first row of group g, hdr[NG] = the
-// total.  (r1/r2 form: per-word offsets, then uint4 pieces -- two dependent L2 loads per output
-// word, 10% of the warp-stall samples of the (32768,29492) throughput kernel, r2n_tp32k.)
+// consecutive information positions inside one output word ((32768,29492): 1,413 pieces for 922
+// words) -- each a uint2 {lo << 16 | (hi - lo) << 5 | s, destination mask}: the run's bits are
+// bits s.. of the 64-bit pair (beta[hi] : beta[lo]) (hi = lo + 1 when the run crosses a codeword
+// word, else hi = lo and the funnel shift is a rotation).  Output words are taken 32 at a time
+// (group g = words 32g .. 32g+31, one per lane); piece j of every word of a group is one
+// coalesced 256-byte row, so a group's loads are independent of each other; a group holds as
+// many rows as its longest word, rounded up to even (padding pieces have mask 0); hdr[g] = its
+// first row, hdr[NG] = the total.  (r1/r2 form: per-word offsets, then uint4 pieces -- two
+// dependent L2 loads per output word, 10% of the warp-stall samples of the (32768,29492)
+// throughput kernel, profiles/r2n_tp32k.txt.)
 __host__ __device__ constexpr int gather_hdr_words(int N, int K) {
     return (((K + 31) / 32 + 31) / 32 + 1 + 3) & ~3;
+}
+PD_INLINE uint32_t gather_piece(const uint32_t* beta, uint2 d) {
+    const uint32_t lo = d.x >> 16, hi = lo + ((d.x >> 5) & 1u);
+    return __funnelshift_r(beta[lo], beta[hi], d.x) & d.y;  // the shift is taken mod 32
 }
 template <int N, int K, int T>
 PD_INLINE void gather_info(const uint32_t* beta, const uint32_t* __restrict__ tab, uint32_t* stg,
@@ -1375,23 +1381,24 @@ PD_INLINE void gather_info(const uint32_t* beta, const uint32_t* __restrict__ ta
     constexpr int NG = (NWK + 31) / 32;
     constexpr int TB = (2 * NB + 3) & ~3;  // the {imask, prefix} words, padded
     const uint32_t* __restrict__ hdr = tab + TB;
-    const uint2* __restrict__ pcs = reinterpret_cast<const uint2*>(tab + TB + gather_hdr_words(N, K));
-    const int lane = (int)lane_id();
+    const uint2* __restrict__ pcs = reinterpret_cast<const uint2*>(tab + TB + gather_hdr_words(N, K)) + lane_id();
     // the first rows of groups 0..31 in one coalesced load, handed out by shuffles
-    const uint32_t hv = lane <= NG ? __ldg(hdr + lane) : 0u;
-    constexpr int GP = 4;  // rows loaded before any is used
+    const uint32_t hv = lane_id() <= (unsigned)NG ? __ldg(hdr + lane_id()) : 0u;
     for (int g = gtid<T>() >> 5; g < NG; g += T / 32) {
         const int r0 = (int)(g < 32 ? __shfl_sync(FULL, hv, g) : __ldg(hdr + g));
         const int r1 = (int)(g + 1 < 32 ? __shfl_sync(FULL, hv, g + 1) : __ldg(hdr + g + 1));
+        const uint2* p = pcs + 32 * r0;
         uint32_t acc = 0;
-        for (int r = r0; r < r1; r += GP) {
-            uint2 d[GP];
-#pragma unroll
-            for (int u = 0; u < GP; ++u) d[u] = r + u < r1 ? __ldg(pcs + (r + u) * 32 + lane) : make_uint2(0u, 0u);
-#pragma unroll
-            for (int u = 0; u < GP; ++u) acc |= __funnelshift_l(beta[d[u].x >> 5], beta[d[u].x >> 5], d[u].x & 31u) & d[u].y;
+        int r = r0;
+        for (; r + 4 <= r1; r += 4, p += 128) {  // four rows in flight
+            const uint2 d0 = __ldg(p), d1 = __ldg(p + 32), d2 = __ldg(p + 64), d3 = __ldg(p + 96);
+            acc |= gather_piece(beta, d0) | gather_piece(beta, d1) | gather_piece(beta, d2) | gather_piece(beta, d3);
         }
-        const int q = 32 * g + lane;
+        if (r < r1) {  // rows come in pairs
+            const uint2 d0 = __ldg(p), d1 = __ldg(p + 32);
+            acc |= gather_piece(beta, d0) | gather_piece(beta, d1);
+        }
+        const int q = 32 * g + (int)lane_id();
         if (q < NWK) out[q] = acc;
     }
 }

@@ -373,10 +373,7 @@ __global__ void __launch_bounds__(GB_T) k_generic_big(const void* __restrict__ l
         for (int q = tid; q < NWK; q += GB_T) {
             uint32_t acc = 0;
             const int g = q >> 5, r1 = (int)__ldg(hdr + g + 1);
-            for (int r = (int)__ldg(hdr + g); r < r1; ++r) {
-                const uint2 d = __ldg(pcs + r * 32 + (q & 31));
-                acc |= __funnelshift_l(beta[d.x >> 5], beta[d.x >> 5], d.x & 31u) & d.y;
-            }
+            for (int r = (int)__ldg(hdr + g); r < r1; ++r) acc |= gather_piece(beta, __ldg(pcs + r * 32 + (q & 31)));
             out[f * NWK + q] = acc;
         }
         __syncthreads();

@@ -416,30 +416,31 @@ static polar_status init_device(polar_code* h) {
         acc += (uint32_t)__builtin_popcount(w);
     }
     // Piece table of the gather (decoder.cuh gather_info, generic.cu): output word q of x_hat[A]
-    // is the OR of its pieces -- maximal runs of information positions that stay in one codeword
-    // word and one output word -- each a uint2 {codeword word << 5 | rotation, destination mask}
-    // with rotation = (destination - source shift) mod 32.  Output words go in groups of 32 (one
-    // per lane); group g owns rows hdr[g] .. hdr[g+1]-1, as many as its longest word, and piece j
-    // of word 32g + l is element l of row hdr[g] + j (padding: {0, 0}).  Layout after the two
+    // is the OR of its pieces -- maximal runs of consecutive information positions inside one
+    // output word -- each a uint2 {lo << 16 | (hi - lo) << 5 | s, destination mask}: the run's
+    // source bits are bits s.. of the pair (beta[hi] : beta[lo]) (a run starting at bit a of word
+    // lo lands at output bit d: s = (a - d) mod 32; hi = lo + 1 when it crosses into the next
+    // word, which implies a > d).  Output words go in groups of 32 (one per lane); group g owns
+    // rows hdr[g] .. hdr[g+1]-1, as many as its longest word rounded up to even, and piece j of
+    // word 32g + l is element l of row hdr[g] + j (padding: {0, 0}).  Layout after the two
     // tables above: hdr[NG + 1] padded to 4 words (gather_hdr_words), then the rows.
     {
         const uint32_t nwk = words_of(h->K), ng = (nwk + 31) / 32;
         std::vector<std::vector<std::pair<uint32_t, uint32_t>>> pw(nwk);
         for (uint32_t j = 0; j < (uint32_t)pos.size();) {
-            const uint32_t q = j / 32, src = pos[j], k = src / 32;
+            const uint32_t q = j / 32, src = pos[j];
             uint32_t len = 1;
-            while (j + len < (uint32_t)pos.size() && (j + len) / 32 == q && pos[j + len] == src + len && (src + len) / 32 == k)
-                ++len;
-            const uint32_t d = j % 32, rot = (d - src % 32) & 31u;
+            while (j + len < (uint32_t)pos.size() && (j + len) / 32 == q && pos[j + len] == src + len) ++len;
+            const uint32_t d = j % 32, a = src % 32, lo = src / 32, cross = a + len > 32 ? 1u : 0u;
             const uint32_t m = (len >= 32 ? 0xffffffffu : ((1u << len) - 1u)) << d;
-            pw[q].push_back({(k << 5) | rot, m});
+            pw[q].push_back({(lo << 16) | (cross << 5) | ((a - d) & 31u), m});
             j += len;
         }
         std::vector<uint32_t> hdr(ng + 1, 0);
         for (uint32_t g = 0; g < ng; ++g) {
             size_t mx = 0;
             for (uint32_t q = 32 * g; q < std::min(nwk, 32 * g + 32); ++q) mx = std::max(mx, pw[q].size());
-            hdr[g + 1] = hdr[g] + (uint32_t)mx;
+            hdr[g + 1] = hdr[g] + (uint32_t)((mx + 1) & ~(size_t)1);
         }
         while (hdr.size() % 4) hdr.push_back(0);
         while (gt.size() % 4) gt.push_back(0);
