@@ -62,7 +62,8 @@ struct Spec {
                           // measured 162/262/207 Gbps at (2048,1723), profiles/r1_history.md)
     int xwpc = 1;         // frame-interleaved variant: warps per CTA (XWPC=)
     bool mailbox = false; // batch-1 persistent mailbox kernel of the int8 latency variant (MAILBOX=1)
-    bool fuse = true;     // CTA-level X<n> and its split child's first op as one fused op (FUSE=0 disables)
+    int fuse = 3;         // CTA-level fused descents: X<n> and the first ops of up to FUSE-1 split
+                          // descendants as one op (FUSE=2: pairs, FUSE=0/1: none)
 };
 
 // Distinct small-subtree patterns emitted once as __noinline__ device functions, so that the
@@ -431,7 +432,7 @@ struct CtaEmitter {
     // State space (SP_GLOBAL 0 / SP_SHARED 1) of a stage, as a placeholder (see stage()).
     std::string space(int m) { return "@P" + std::to_string(m) + "@"; }
 
-    void child(int id, const std::string& src, bool first_done = false) {
+    void child(int id, const std::string& src, int done = 0) {
         const Node& v = t.nodes[id];
         if (v.kind == Kind::Rate0) return;  // beta zeroed at frame start
         if (v.n > W && v.n <= XW && !in_region) {
@@ -443,7 +444,7 @@ struct CtaEmitter {
             emit("sync();");
             return;
         }
-        if (v.n > W) cta(id, src, first_done);
+        if (v.n > W) cta(id, src, done);
         else sub_call(id, src);
     }
 
@@ -451,6 +452,7 @@ struct CtaEmitter {
     // G_0R when c's left child is Rate-0) as one op, when c is a CTA-level split node outside a
     // warp-0 region.  Returns the child's first-op kind (OP_F 0, OP_G0R 2) or -1.
     bool fuse = false;
+    int fuse_depth = 3;  // FUSE=2: pairs only
     int fuse_kind(int cid) {
         if (!fuse) return -1;
         const Node& c = t.nodes[cid];
@@ -478,16 +480,33 @@ struct CtaEmitter {
             return;
         }
         const std::string D2 = stage(h / 2);
+        const std::string BB = XK == 1 ? B : std::string("beta");
+        const Node& c = t.nodes[cid];
+        const int gcid = YK == 0 ? c.left : c.right;
+        const int ZK = fuse_depth >= 3 ? fuse_kind(gcid) : -1;
+        if (ZK >= 0) {
+            const std::string D3 = stage(h / 4);
+            emit("cXYZ<P, T, " + N_ + ", " + CL + ", " + std::to_string(XK) + ", " + std::to_string(YK) + ", " +
+                 std::to_string(ZK) + ", " + SS + ", " + space(h) + ", " + space(h / 2) + ", " + space(h / 4) + ", NI>(" + src +
+                 ", " + D + ", " + D2 + ", " + D3 + ", " + BB + ");");
+            emit("sync();");
+            emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
+            emit("PD_DUMPS(" + D2 + ", " + std::to_string(h / 2) + ");");
+            emit("PD_DUMPS(" + D3 + ", " + std::to_string(h / 4) + ");");
+            if (id == 0 && XK != 0) emit("sync.root_g_done();");
+            child(cid, D, 2);
+            return;
+        }
         emit("cXY<P, T, " + N_ + ", " + CL + ", " + std::to_string(XK) + ", " + std::to_string(YK) + ", " + SS + ", " +
-             space(h) + ", " + space(h / 2) + ", NI>(" + src + ", " + D + ", " + D2 + ", " + (XK == 1 ? B : std::string("beta")) + ");");
+             space(h) + ", " + space(h / 2) + ", NI>(" + src + ", " + D + ", " + D2 + ", " + BB + ");");
         emit("sync();");
         emit("PD_DUMPS(" + D + ", " + std::to_string(h) + ");");
         emit("PD_DUMPS(" + D2 + ", " + std::to_string(h / 2) + ");");
         if (id == 0 && XK != 0) emit("sync.root_g_done();");
-        child(cid, D, true);
+        child(cid, D, 1);
     }
 
-    void cta(int id, const std::string& src, bool first_done = false) {
+    void cta(int id, const std::string& src, int done = 0) {
         const std::string SS = src == "chan" ? "CHS" : space(t.nodes[id].n);
         const Node& v = t.nodes[id];
         const int n = v.n;
@@ -516,11 +535,12 @@ struct CtaEmitter {
         const std::string D = stage(h);
         const Node& l = t.nodes[v.left];
         const Node& r = t.nodes[v.right];
-        // first_done: this node's first op (G_0R or F) ran fused into its parent's op
+        // done > 0: this node's first op (G_0R or F) ran fused into an ancestor's op, and so did the
+        // first ops of done - 1 further nodes down its first-child chain
         // HELPER: one arrive per subtree call, just before the stage op that produces its input
         if (l.kind == Kind::Rate0) {
-            if (first_done) {
-                child(v.right, D);
+            if (done > 0) {
+                child(v.right, D, done - 1);
             } else {
                 if (helper && h == W && r.kind != Kind::Rate0) emit("if (gtid<T>() < 32) sync.helper_arrive();");
                 xop_child(id, 2, src, D, B, v.right);
@@ -529,8 +549,8 @@ struct CtaEmitter {
             emit("sync.comb();");
             return;
         }
-        if (first_done) {
-            child(v.left, D);
+        if (done > 0) {
+            child(v.left, D, done - 1);
         } else {
             if (helper && h == W) emit("if (gtid<T>() < 32) sync.helper_arrive();");
             xop_child(id, 0, src, D, B, v.left);
@@ -767,7 +787,8 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         ce.XW = sp.xw;
         ce.helper = sp.helper > 0;
         ce.latni = sp.latni;
-        ce.fuse = sp.fuse && !ce.helper;
+        ce.fuse = sp.fuse >= 2 && !ce.helper;
+        ce.fuse_depth = sp.fuse;
         int acc = 0, sacc = 0, gacc = 0, hs = 0, hg = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         ce.h16 = sp.h16;
@@ -1075,7 +1096,7 @@ void parse_options(Spec& sp, std::istream& ls) {
             else if (opt.rfind("XSM=", 0) == 0) sp.xsm = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("XWPC=", 0) == 0) sp.xwpc = std::atoi(opt.c_str() + 5);
             else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;
-            else if (opt.rfind("FUSE=", 0) == 0) sp.fuse = std::atoi(opt.c_str() + 5) != 0;
+            else if (opt.rfind("FUSE=", 0) == 0) sp.fuse = std::atoi(opt.c_str() + 5);
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();
                 std::stringstream ds(opt.substr(6));

@@ -1072,6 +1072,52 @@ PD_INLINE void cXY(const TS* src, TD* dst, TD2* dst2, const uint32_t* beta) {
     else cXY_body<P, T, n, CLAMP, XK, YK, SS, DS, DS2, TS, TD, TD2>(src, dst, dst2, beta);
 }
 
+// Three-level fused descent: X<n>, then Y<n/2> on X's outputs, then Z<n/4> on Y's outputs (Y, Z:
+// F, or G_0R when the node's left child is Rate-0), all CTA-level.  Element i of Z's output needs
+// node values i + k n/8 (k = 0..7): eight chunk loads per thread, the X, Y and Z outputs stored
+// (each is the alpha of a node whose G reads it later), none re-read.
+template <class P, int T, int n, bool CLAMP, int XK, int YK, int ZK, int SS, int DS, int DS2, int DS3, class S, class D,
+          class D2, class D3>
+PD_INLINE void cXYZ_body(const void* src, void* dst, void* dst2, void* dst3, const uint32_t* beta) {
+    constexpr int R = n / 8, CE = chunk_elems<P, R, T>(), STEP = CE * T;
+    constexpr int LH = CLAMP ? L2_FIRST : L2_LAST;
+#pragma unroll 1
+    for (int i = CE * gtid<T>(); i < R; i += STEP) {
+        Chunk<P, CE> a[4], b[4];
+        uint32_t bits[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            a[k].template load_raw<SS, LH>((const S*)src + i + k * R);
+            b[k].template load_raw<SS, LH>((const S*)src + i + k * R + 4 * R);
+            bits[k] = XK == OP_G ? beta[(i + k * R) >> 5] >> ((i + k * R) & 31) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            a[k].template unpack_raw<S>(CLAMP);
+            b[k].template unpack_raw<S>(CLAMP);
+            chunk_op<XK>(a[k], b[k], bits[k]);
+            a[k].template store<DS, L2_LAST>((D*)dst + i + k * R);
+        }
+        chunk_op<YK>(a[0], a[2], 0u);
+        a[0].template store<DS2, L2_LAST>((D2*)dst2 + i);
+        chunk_op<YK>(a[1], a[3], 0u);
+        a[1].template store<DS2, L2_LAST>((D2*)dst2 + i + R);
+        chunk_op<ZK>(a[0], a[1], 0u);
+        a[0].template store<DS3, L2_LAST>((D3*)dst3 + i);
+    }
+}
+template <class P, int T, int n, bool CLAMP, int XK, int YK, int ZK, int SS, int DS, int DS2, int DS3, class S, class D,
+          class D2, class D3>
+__device__ __noinline__ void cXYZ_impl(const void* src, void* dst, void* dst2, void* dst3, const uint32_t* beta) {
+    cXYZ_body<P, T, n, CLAMP, XK, YK, ZK, SS, DS, DS2, DS3, S, D, D2, D3>(src, dst, dst2, dst3, beta);
+}
+template <class P, int T, int n, bool CLAMP, int XK, int YK, int ZK, int SS, int DS, int DS2, int DS3, bool NI, class TS,
+          class TD, class TD2, class TD3>
+PD_INLINE void cXYZ(const TS* src, TD* dst, TD2* dst2, TD3* dst3, const uint32_t* beta) {
+    if constexpr (NI) cXYZ_impl<P, T, n, CLAMP, XK, YK, ZK, SS, DS, DS2, DS3, TS, TD, TD2, TD3>(src, dst, dst2, dst3, beta);
+    else cXYZ_body<P, T, n, CLAMP, XK, YK, ZK, SS, DS, DS2, DS3, TS, TD, TD2, TD3>(src, dst, dst2, dst3, beta);
+}
+
 template <class P, int T, int n, bool CLAMP, int SS, int DS, class S, class D>
 __device__ __noinline__ void cF_impl(const void* src, void* dst) {
     cF_body<P, T, n, CLAMP, SS, DS, S, D>(src, dst);
