@@ -1430,6 +1430,34 @@ PD_INLINE void gather_info(const uint32_t* beta, const uint32_t* __restrict__ ta
     const uint2* __restrict__ pcs = reinterpret_cast<const uint2*>(tab + TB + gather_hdr_words(N, K)) + lane_id();
     // the first rows of groups 0..31 in one coalesced load, handed out by shuffles
     const uint32_t hv = lane_id() <= (unsigned)NG ? __ldg(hdr + lane_id()) : 0u;
+    if constexpr (T == 32 && NG >= 4 && NG < 32) {  // (2048,1723), NG = 2: the per-group loop measured faster
+        // one warp takes every group: the rows of all groups are consecutive, so they stream
+        // through a register window PF rows ahead across group boundaries (a group's word is
+        // complete when its last row pair has been consumed); no load waits on a computation
+        constexpr int PF = 8;
+        const int total = (int)__shfl_sync(FULL, hv, NG);
+        uint2 d[PF];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) d[u] = u < total ? __ldg(pcs + 32 * u) : make_uint2(0u, 0u);
+        const uint2* p = pcs + 32 * PF;
+        int gi = 0, gend = (int)__shfl_sync(FULL, hv, 1);
+        uint32_t acc = 0;
+        for (int r = 0; r < total; r += 2, p += 64) {
+            acc |= gather_piece(beta, d[0]) | gather_piece(beta, d[1]);
+#pragma unroll
+            for (int u = 0; u < PF - 2; ++u) d[u] = d[u + 2];
+            d[PF - 2] = r + PF < total ? __ldg(p) : make_uint2(0u, 0u);
+            d[PF - 1] = r + PF + 1 < total ? __ldg(p + 32) : make_uint2(0u, 0u);
+            if (r + 2 == gend) {
+                const int q = 32 * gi + (int)lane_id();
+                if (q < NWK) out[q] = acc;
+                acc = 0;
+                ++gi;
+                gend = (int)__shfl_sync(FULL, hv, gi + 1);
+            }
+        }
+        return;
+    }
     for (int g = gtid<T>() >> 5; g < NG; g += T / 32) {
         const int r0 = (int)(g < 32 ? __shfl_sync(FULL, hv, g) : __ldg(hdr + g));
         const int r1 = (int)(g + 1 < 32 ? __shfl_sync(FULL, hv, g + 1) : __ldg(hdr + g + 1));
