@@ -49,6 +49,7 @@ struct Spec {
     int ll = 0;           // lane-local tiny subtrees up to this size (LL=8 enables; measured slower, profiles/r1_history.md)
     int cps = 1;          // throughput variant: CTAs per SM requested from ptxas (__launch_bounds__ min blocks)
     int wlat = 0;         // latency variant's warp-subtree size (WLAT=; default W)
+    int wf = 0;           // f32 throughput variant's warp-subtree size (WF=; default W)
     int xw = 0;           // latency variant: CTA-level nodes up to XW run on warp 0 alone (XW=)
     int helper = 0;       // latency variant: run-ahead helper warp on scheduler HELPER-1 (HELPER=1|2)
     bool latni = false;   // latency variant: non-inlined subtree copies (LATNI=1)
@@ -840,6 +841,10 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     };
     const int WL = std::min(sp.N, sp.wlat > 0 ? sp.wlat : W);
     const bool two = WL != W;
+    // WF: the f32 throughput variant may want another subtree size than the int8 one (its
+    // stages are 4x larger: (2048,1723) int8 is fastest at W = 512, f32 at W = 2048)
+    const int WF = std::min(sp.N, sp.wf > 0 ? sp.wf : W);
+    const bool three = WF != W && WF != WL;
     if (two) {
         g_marks = nullptr;  // trace marks belong to the latency variant's code
         emit_struct("Code", W);
@@ -847,6 +852,12 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         emit_struct("CodeLat", WL);
     } else {
         emit_struct("Code", W);
+    }
+    if (three) {
+        TraceMarks* keep = g_marks;
+        g_marks = nullptr;
+        emit_struct("CodeF", WF);
+        g_marks = keep;
     }
     // frame-interleaved variant: the largest stages go to the global slot until the shared
     // stages (and beta, unless it is global too) fit the per-warp budget
@@ -875,6 +886,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     }
     const std::string C = "pd::code_" + sp.name + "::Code";
     const std::string CL = "pd::code_" + sp.name + (two ? "::CodeLat" : "::Code");
+    const std::string CF = "pd::code_" + sp.name + (WF == W ? "::Code" : WF == WL ? "::CodeLat" : "::CodeF");
     const int t_lat = sp.N > WL ? sp.T : 32;
     struct V {
         const char* tag;
@@ -891,21 +903,33 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     // Throughput variant: as many lockstep warps (frames) per CTA as the shared memory of one
     // SM holds, at most 16 (same formula as FrameLayout::PER_FRAME).
     auto a16 = [](int x) { return (x + 15) & ~15; };
-    int g_elems = 0, h_smem = 0, h_glob = 0;  // H16 layout bytes (as emit_struct computes them)
-    if (cta_phase) {
-        const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
-        for (int m = sp.N / 2; m >= W; m /= 2) {
-            const int hb = m * (m <= sp.h16 ? 2 : 1);
-            if (m >= gs) g_elems += m, h_glob += hb;
-            else h_smem += hb;
+    // stage element counts of a struct with warp-subtree size Wv (as emit_struct computes them)
+    struct SL {
+        bool cta;
+        int g_elems = 0, h_smem = 0, h_glob = 0;  // global stage elements; H16 layout bytes
+    };
+    auto layout_of = [&](int Wv) {
+        SL l{sp.N > Wv};
+        if (l.cta) {
+            const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
+            for (int m = sp.N / 2; m >= Wv; m /= 2) {
+                const int hb = m * (m <= sp.h16 ? 2 : 1);
+                if (m >= gs) l.g_elems += m, l.h_glob += hb;
+                else l.h_smem += hb;
+            }
         }
-    }
+        return l;
+    };
+    const SL lw = layout_of(W), lf = layout_of(WF);
+    const int g_elems = lw.g_elems, h_glob = lw.h_glob;
     const bool h16 = cta_phase && sp.h16 > 0;
     auto fpc = [&](const char* prof, bool chan_smem) {
         const int s = std::string(prof) == "PF32" ? 4 : 1;
-        const int stages = (h16 && s == 1) ? a16(h_smem) : a16(std::max(0, cta_phase ? sp.N - W - g_elems : 0) * s);
+        const SL& l = s == 4 ? lf : lw;
+        const int Wv = s == 4 ? WF : W;
+        const int stages = (h16 && s == 1) ? a16(l.h_smem) : a16(std::max(0, l.cta ? sp.N - Wv - l.g_elems : 0) * s);
         const int outw = a16((sp.K + 31) / 32 * 4);
-        const bool gb = sp.gbeta && g_elems > 0;
+        const bool gb = sp.gbeta && l.g_elems > 0;
         const int per = (chan_smem ? 2 * a16(sp.N * s) : 0) + stages + (gb ? 0 : a16(std::max(1, sp.N / 32) * 4)) +
                         (stages >= outw ? 0 : outw) + 16;
         return std::max(1, std::min(sp.fpc_max, (220 * 1024) / per));
@@ -913,7 +937,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     const bool cs_f = 2 * bytes("PF32") <= 16384, cs_i = 2 * bytes("PI8") <= 16384;
     const bool gt = g_elems > 0;
     std::vector<V> vars = {
-        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f), gt, 1, false, false},
+        {"tp_f32", "PF32", 32, cs_f, fpc("PF32", cs_f), lf.g_elems > 0, 1, false, false},
         {"tp_i8", "PI8", 32, cs_i, fpc("PI8", cs_i), gt, sp.cps, false, h16},
         {"lat_f32", "PF32", t_lat, bytes("PF32") <= 32768, 1, false, 1, true, false},
         {"lat_i8", "PI8", t_lat, bytes("PI8") <= 32768, 1, false, 1, true, false},
@@ -921,13 +945,15 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
     // the host-side registry symbols exist only in the build-time (nvcc) compilation
     o << "#ifndef __CUDACC_RTC__\n";
     auto gscratch_of = [&](const V& v) {
-        return v.gtop ? (v.h16 ? a16(h_glob) : a16(g_elems * (std::string(v.prof) == "PF32" ? 4 : 1))) +
+        const bool f = std::string(v.prof) == "PF32" && !v.lat;
+        return v.gtop ? (v.h16 ? a16(h_glob) : a16((f ? lf.g_elems : g_elems) * (std::string(v.prof) == "PF32" ? 4 : 1))) +
                             (sp.gbeta ? a16(std::max(1, sp.N / 32) * 4) : 0)
                       : 0;
     };
     int vi = 0;
     for (auto& v : vars) {
-        const std::string targs = std::string("pd::") + v.prof + ", " + (v.lat ? CL : C) + ", " + std::to_string(v.T) + ", " +
+        const std::string cs = v.lat ? CL : std::string(v.prof) == "PF32" ? CF : C;
+        const std::string targs = std::string("pd::") + v.prof + ", " + cs + ", " + std::to_string(v.T) + ", " +
                                   std::to_string(v.fpc) + ", " + (v.chan_smem ? "true" : "false") + ", " +
                                   (v.gtop ? "true" : "false") + ", " + (v.h16 ? "true" : "false");
         const std::string kargs = targs + ", " + std::to_string(v.minb);
@@ -1089,6 +1115,7 @@ void parse_options(Spec& sp, std::istream& ls) {
             else if (opt.rfind("LL=", 0) == 0) sp.ll = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("CPS=", 0) == 0) sp.cps = std::atoi(opt.c_str() + 4);
             else if (opt.rfind("WLAT=", 0) == 0) sp.wlat = std::atoi(opt.c_str() + 5);
+            else if (opt.rfind("WF=", 0) == 0) sp.wf = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("XW=", 0) == 0) sp.xw = std::atoi(opt.c_str() + 3);
             else if (opt.rfind("HELPER=", 0) == 0) sp.helper = std::atoi(opt.c_str() + 7);
             else if (opt.rfind("LATNI=", 0) == 0) sp.latni = std::atoi(opt.c_str() + 6) != 0;
