@@ -366,12 +366,12 @@ struct CtaEmitter {
     static std::string region(std::string x) {
         for (size_t q; (q = x.find("<P, T, ")) != std::string::npos;) x.replace(q, 7, "<P, 32, ");
         for (size_t q; (q = x.find("<T, ")) != std::string::npos;) x.replace(q, 4, "<32, ");
-        if (x == "sync();" || x == "sync.comb();") x = "__syncwarp();";
+        if (x == "sync();" || x == "sync.comb();" || x == "sync.sub();") x = "__syncwarp();";
         return x;
     }
     void emit(const std::string& stmt0) {
         const std::string stmt = in_region ? region(stmt0) : stmt0;
-        if ((stmt == "sync();" || stmt == "sync.comb();" || stmt == "__syncwarp();") && g_marks) {
+        if ((stmt == "sync();" || stmt == "sync.comb();" || stmt == "sync.sub();" || stmt == "__syncwarp();") && g_marks) {
             emit_raw(stmt);
             std::string lab = last_op.rfind("if (gtid", 0) == 0 ? std::string("subtree") : last_op.substr(0, last_op.find('('));
             emit_raw(g_marks->mark("cta:" + lab));
@@ -427,7 +427,7 @@ struct CtaEmitter {
             emit_warp_sub(subs, t, id, fname, sh);
             emit("if (w0) " + fname + "<P>(" + src + ", beta);");
         }
-        emit("sync();");
+        emit("sync.sub();");
     }
 
     // State space (SP_GLOBAL 0 / SP_SHARED 1) of a stage, as a placeholder (see stage()).

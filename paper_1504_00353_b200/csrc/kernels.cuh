@@ -47,6 +47,15 @@ struct OpSync {
         if constexpr (T > 32) asm volatile("bar.sync 1, %0;" ::"n"(T) : "memory");
         else asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
     }
+    // the frame group's barrier regardless of lockstep (the shared frame hand-out)
+    PD_INLINE void group() const {
+        if constexpr (T > 32) asm volatile("bar.sync 1, %0;" ::"n"(T) : "memory");
+        else asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
+    }
+    // after a warp subtree call: the full op barrier -- without it the throughput warps drift
+    // apart and stop sharing instruction fetch (measured: no lockstep at all 433 -> 320 Gbps,
+    // lockstep everywhere but here 433 -> 435, profiles/r1_history.md)
+    PD_INLINE void sub() const { (*this)(); }
     // after a Combine (a few word XORs on the group's own decision bits): in the throughput
     // variant only the warp's own lanes need to see them, so the frame group is not held in
     // lockstep there (+0.3%, same-box A/B)
@@ -239,8 +248,9 @@ __global__ void __launch_bounds__(T * FPC + (T > 32 ? 32 * C::HELPER : 0), MINB)
         }
         if constexpr (DYN) {
             if (threadIdx.x == 0) s_next = ((long long)gridDim.x + (long long)atomicAdd(gctr, 1ull)) * FPC;
-            sync();
+            sync.group();
             f = s_next + grp;
+            sync.group();  // every warp has read s_next before warp 0 may overwrite it
         } else {
             f += stride;
         }
