@@ -1079,43 +1079,65 @@ PD_INLINE void cXY(const TS* src, TD* dst, TD2* dst2, const uint32_t* beta) {
 // The int8 channel versions (the two root ops, streaming the frame from HBM) are software-
 // pipelined: the eight 8-byte chunks of the next step are loaded before the current step is
 // computed, so each HBM round trip overlaps the previous step's work.
+// one step of cXYZ_pipe: compute the chunks in raw (step at i), after refilling raw with the
+// step PD steps later (its loads stay in flight while this step computes)
+template <class P, int n, bool CLAMP, int XK, int YK, int ZK, int DS, int DS2, int DS3, int PD, class S, class D, class D2,
+          class D3>
+PD_INLINE void cXYZ_pipe_step(int i, uint32_t (&raw)[8][2], const void* src, void* dst, void* dst2, void* dst3,
+                              const uint32_t* beta) {
+    constexpr int R = n / 8, CE = 8, STEP = CE * 32;
+    constexpr int LH = CLAMP ? L2_FIRST : L2_LAST;
+    Chunk<P, CE> a[4], b[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        a[k].w[0] = raw[k][0];
+        a[k].w[1] = raw[k][1];
+        b[k].w[0] = raw[k + 4][0];
+        b[k].w[1] = raw[k + 4][1];
+    }
+    if (i + PD * STEP < R) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            vld<SP_GLOBAL, 8, LH>((const S*)src + i + PD * STEP + (k & 3) * R + (k >> 2) * 4 * R, raw[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t bits = XK == OP_G ? beta[(i + k * R) >> 5] >> ((i + k * R) & 31) : 0u;
+        a[k].template unpack_raw<S>(CLAMP);
+        b[k].template unpack_raw<S>(CLAMP);
+        chunk_op<XK>(a[k], b[k], bits);
+        a[k].template store<DS, L2_LAST>((D*)dst + i + k * R);
+    }
+    chunk_op<YK>(a[0], a[2], 0u);
+    a[0].template store<DS2, L2_LAST>((D2*)dst2 + i);
+    chunk_op<YK>(a[1], a[3], 0u);
+    a[1].template store<DS2, L2_LAST>((D2*)dst2 + i + R);
+    chunk_op<ZK>(a[0], a[1], 0u);
+    a[0].template store<DS3, L2_LAST>((D3*)dst3 + i);
+}
 template <class P, int n, bool CLAMP, int XK, int YK, int ZK, int DS, int DS2, int DS3, class S, class D, class D2, class D3>
 PD_INLINE void cXYZ_pipe(const void* src, void* dst, void* dst2, void* dst3, const uint32_t* beta) {
     constexpr int R = n / 8, CE = 8, STEP = CE * 32;
     constexpr int LH = CLAMP ? L2_FIRST : L2_LAST;
-    uint32_t raw[8][2];  // the chunks of the next step: k = 0..3 (node values i + kR), 4..7 (+ 4R)
+#ifndef POLAR_PIPE_DEPTH
+#define POLAR_PIPE_DEPTH 1  // 2: two steps in flight (measured: 500 bytes of spills in the kernel)
+#endif
+    constexpr int PD = (POLAR_PIPE_DEPTH == 2 && R / STEP >= 2 && (R / STEP) % 2 == 0) ? 2 : 1;
+    // the chunks of the next PD steps: k = 0..3 (node values i + kR), 4..7 (+ 4R)
+    uint32_t raw0[8][2], raw1[8][2];
     int i = CE * (int)lane_id();
 #pragma unroll
-    for (int k = 0; k < 8; ++k) vld<SP_GLOBAL, 8, LH>((const S*)src + i + (k & 3) * R + (k >> 2) * 4 * R, raw[k]);
+    for (int k = 0; k < 8; ++k) vld<SP_GLOBAL, 8, LH>((const S*)src + i + (k & 3) * R + (k >> 2) * 4 * R, raw0[k]);
+    if constexpr (PD == 2) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            vld<SP_GLOBAL, 8, LH>((const S*)src + i + STEP + (k & 3) * R + (k >> 2) * 4 * R, raw1[k]);
+    }
 #pragma unroll 1
-    for (; i < R; i += STEP) {
-        Chunk<P, CE> a[4], b[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            a[k].w[0] = raw[k][0];
-            a[k].w[1] = raw[k][1];
-            b[k].w[0] = raw[k + 4][0];
-            b[k].w[1] = raw[k + 4][1];
-        }
-        if (i + STEP < R) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                vld<SP_GLOBAL, 8, LH>((const S*)src + i + STEP + (k & 3) * R + (k >> 2) * 4 * R, raw[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t bits = XK == OP_G ? beta[(i + k * R) >> 5] >> ((i + k * R) & 31) : 0u;
-            a[k].template unpack_raw<S>(CLAMP);
-            b[k].template unpack_raw<S>(CLAMP);
-            chunk_op<XK>(a[k], b[k], bits);
-            a[k].template store<DS, L2_LAST>((D*)dst + i + k * R);
-        }
-        chunk_op<YK>(a[0], a[2], 0u);
-        a[0].template store<DS2, L2_LAST>((D2*)dst2 + i);
-        chunk_op<YK>(a[1], a[3], 0u);
-        a[1].template store<DS2, L2_LAST>((D2*)dst2 + i + R);
-        chunk_op<ZK>(a[0], a[1], 0u);
-        a[0].template store<DS3, L2_LAST>((D3*)dst3 + i);
+    for (; i < R; i += PD * STEP) {
+        cXYZ_pipe_step<P, n, CLAMP, XK, YK, ZK, DS, DS2, DS3, PD, S, D, D2, D3>(i, raw0, src, dst, dst2, dst3, beta);
+        if constexpr (PD == 2)
+            cXYZ_pipe_step<P, n, CLAMP, XK, YK, ZK, DS, DS2, DS3, PD, S, D, D2, D3>(i + STEP, raw1, src, dst, dst2, dst3, beta);
     }
 }
 template <class P, int T, int n, bool CLAMP, int XK, int YK, int ZK, int SS, int DS, int DS2, int DS3, class S, class D,
