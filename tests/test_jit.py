@@ -26,8 +26,11 @@ def _expected(mask, x):
     return oracle.pack_bits(oracle.info_bits(mask, oracle.fastssc_decode(mask, x, threads=os.cpu_count() or 1)))
 
 
+# ga_32768_32000: ceil(K/32) = 1000 output words = 32 groups of the gather's piece table, so the
+# gather takes its per-group path with a header load past the first 32 groups (decoder.cuh
+# gather_info) in both kernel variants
 JIT_CODES = [("random_1024_600", 1024, 600, None, 2.5), ("ga_4096_2048_at_3dB", 4096, 2048, 3.0, 3.0),
-             ("ga_32768_29492_at_4dB", 32768, 29492, 4.0, 4.5)]
+             ("ga_32768_29492_at_4dB", 32768, 29492, 4.0, 4.5), ("ga_32768_32000_at_6dB", 32768, 32000, 6.0, 6.5)]
 
 
 @pytest.mark.gpu
