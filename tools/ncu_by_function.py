@@ -32,7 +32,7 @@ def main():
     per, cur, line = Counter(), "?", None
     samp = Counter()
     reasons = {}
-    hdr = None
+    hdr, sidx = None, []
     total = 0
     by_addr = {}  # an inlined instruction is listed under every source line of its inline chain
     with gzip.open(a.prefix + "_source.csv.gz", "rt") as f:
@@ -42,8 +42,9 @@ def main():
             if r[0] == "File Path":
                 cur = r[1].split("/")[-1]
                 continue
-            if r[0] == "Line No":
-                hdr = [h.replace("stall_", "") for h in r[31:48]]
+            if r[0] == "Line No":  # the stall-reason columns (all samples, not the not-issued copies)
+                sidx = [i for i, h in enumerate(r) if h.startswith("stall_") and "Not Issued" not in h]
+                hdr = [r[i].replace("stall_", "") for i in sidx]
             if r[0] in ("Function Name", "Line No") or len(r) < 8:
                 continue
             if r[0]:
@@ -53,7 +54,7 @@ def main():
                 try:
                     n = int(r[7] or 0)
                     smp = int(r[4] or 0)
-                    why = [int(x or 0) for x in r[31:48]] if hdr and len(r) >= 48 else []
+                    why = [int(r[i] or 0) for i in sidx] if hdr else []
                 except ValueError:
                     continue
                 if cur in maps and line:
