@@ -546,12 +546,16 @@ PD_INLINE void wG(const Src& s, typename P::v_t* c, uint64_t bw, uint32_t ml) {
         const bool second = lane_id() & (n / 2);
         c[0] = P::g(second ? y : x, second ? x : y, (ml >> (lane_id() & (n / 2 - 1))) & 1u);
 #else
-        const uint32_t sgn = ((ml >> (lane_id() & (n / 2 - 1))) & 1u) << 31;
-        const uint32_t second = (lane_id() & (n / 2)) ? 0xffffffffu : 0u;
+        // sgn: beta of this lane's element at bit 31 only; sec: the lane's "second half" bit
+        // (lane & n/2) shifted to bit 31 (the lower lane bits land below 31, masked by sgn), so
+        // each flip is one three-input LOP3 (no predicate / select)
+        constexpr int LH = n >= 4 ? (n == 4 ? 1 : n == 8 ? 2 : n == 16 ? 3 : n == 32 ? 4 : 0) : 0;
+        const uint32_t sgn = (ml >> (lane_id() & (n / 2 - 1))) << 31;
+        const uint32_t sec = lane_id() << (31 - LH);
         typename P::v_t x, y;
         s.pair(n / 2, x, y);
-        const float xa = __uint_as_float(__float_as_uint(x) ^ (sgn & ~second));
-        const float ya = __uint_as_float(__float_as_uint(y) ^ (sgn & second));
+        const float xa = __uint_as_float(__float_as_uint(x) ^ (sgn & ~sec));
+        const float ya = __uint_as_float(__float_as_uint(y) ^ (sgn & sec));
         c[0] = P::g0(xa, ya);
 #endif
     }
