@@ -629,6 +629,13 @@ PD_INLINE uint32_t wRepm(const Src& s) {
 // least reliable bit, the lowest index among equal magnitudes (reading C10).  int8 profile:
 // the f32 bits of an integer magnitude <= 254 leave the low 16 mantissa bits zero, so
 // (|alpha| bits | index) is one exact key and one redux.min finds both minimum and index.
+// int8 SPC key (|x| f32 bits | element index < 2^16): the low 16 mantissa bits of an integer
+// <= 254 are zero, so the key is one select-LOP3 of the value's bits 16-30 and the index
+PD_INLINE uint32_t spc_key16(float x, uint32_t idx) {
+    uint32_t key;
+    asm("lop3.b32 %0, %1, %2, 0x7fff0000, 0xE4;" : "=r"(key) : "r"(__float_as_uint(x)), "r"(idx));
+    return key;
+}
 template <class P, int n, class Src>
 PD_INLINE uint32_t wSPCm(const Src& s) {
     static_assert(n <= 32, "");
@@ -637,7 +644,12 @@ PD_INLINE uint32_t wSPCm(const Src& s) {
     const uint32_t parity = __popc(hdm) & 1u;
     uint32_t idx;
     if constexpr (P::kPackedKey) {
-        idx = __reduce_min_sync(FULL, P::mag_key(x) | (lane_id() & (n - 1))) & 31u;
+        // (|x| bits with the low log2(n) bits -- zero for an integer <= 254 -- replaced by the
+        // lane's element index): one select-LOP3 instead of mask-then-or
+        constexpr uint32_t KM = 0x7fffffffu & ~(uint32_t)(n - 1);
+        uint32_t key;  // (x & KM) | (lane & ~KM): lane has no bit 31, KM none either
+        asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(key) : "r"(__float_as_uint(x)), "r"(lane_id()), "n"(KM));
+        idx = __reduce_min_sync(FULL, key) & 31u;
     } else {
         const uint32_t key = P::mag_key(x);
         const uint32_t mn = __reduce_min_sync(FULL, key);
@@ -662,7 +674,7 @@ PD_INLINE void wSPC(const Src& s, uint64_t& bw) {
         for (int j = 0; j < J; ++j) {
             const auto x = s.v(j);
             hb |= (HB)P::hd(x) << j;
-            kk[j] = P::mag_key(x) | (uint32_t)(j * 32 + lane_id());
+            kk[j] = spc_key16(x, (uint32_t)(j * 32) | lane_id());
         }
 #pragma unroll
         for (int m = J; m > 1; m /= 2)
@@ -747,7 +759,7 @@ PD_INLINE void wSPC(const Src& s, BW<NW>& bw) {
             const auto x = s.v(j);
             hw[j] = __ballot_sync(FULL, P::hd(x));
             par ^= hw[j];
-            kk[j] = P::mag_key(x) | (uint32_t)(j * 32 + lane_id());
+            kk[j] = spc_key16(x, (uint32_t)(j * 32) | lane_id());
         }
 #pragma unroll
         for (int m = J; m > 1; m /= 2)
