@@ -610,9 +610,18 @@ PD_INLINE bool wRepDecide(const Src& s) {
     } else {
         t0 = P::acc(s.one(n));
     }
+    if constexpr (P::kExactSum) {
+        // int8 profile: the values are integers, so the lane's partial is converted exactly
+        // (1.5 * 2^23 magic) and one redux.sync.add sums the warp: the node's sum (N_v >= 64) or
+        // 32 / N_v copies of it (replicated N_v <= 32) -- the same sign, hence the same decision
+        // (C9, C12) -- one 23-cycle collective instead of log2(N_v) dependent shuffle-adds
+        const int iv = __float_as_int(t0 + 12582912.0f) - 0x4B400000;
+        return __reduce_add_sync(FULL, iv) < 0;
+    } else {
 #pragma unroll
-    for (int o = start; o >= 1; o /= 2) t0 = P::add(t0, __shfl_xor_sync(FULL, t0, o));
-    return P::acc_neg(t0);
+        for (int o = start; o >= 1; o /= 2) t0 = P::add(t0, __shfl_xor_sync(FULL, t0, o));
+        return P::acc_neg(t0);
+    }
 }
 template <class P, int n, int s0, class Src>
 PD_INLINE void wRep(const Src& s, uint64_t& bw) {
