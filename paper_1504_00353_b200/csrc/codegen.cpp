@@ -63,6 +63,8 @@ struct Spec {
                           // measured 162/262/207 Gbps at (2048,1723), profiles/r1_history.md)
     int xwpc = 1;         // frame-interleaved variant: warps per CTA (XWPC=)
     bool mailbox = false; // batch-1 persistent mailbox kernel of the int8 latency variant (MAILBOX=1)
+    bool fcomb = false;   // FCOMB=1: a warp-subtree right child performs its CTA-level parent's Combine
+                          // (measured: (32768,29492) +0.6%, (2048,1723) -1.4%, batch-1 -0.2%: opt-in)
     int fuse = 3;         // CTA-level fused descents: X<n> and the first ops of up to FUSE-1 split
                           // descendants as one op (FUSE=2: pairs, FUSE=0/1: none)
 };
@@ -295,8 +297,11 @@ std::string Emitter::shared_fn(int id) {
 }
 
 // A warp subtree function: root node id, whose input LLRs are at `src` (shared memory).
+// comb: the subtree is the right child of a CTA-level node whose Combine it performs at its end
+// (1: Combine, left words ^= right words; 2: Combine_0R, left words = right words) -- the CTA op
+// and its barrier disappear (decoder.cuh wStoreBetaComb)
 void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::string& fname, SharedFns* sh,
-                   bool chan = false, bool noinline = false) {
+                   bool chan = false, bool noinline = false, int comb = 0) {
     const Node& v = t.nodes[id];
     const int R = v.n;
     o << "    template <class P, class SrcT>\n"
@@ -315,7 +320,11 @@ void emit_warp_sub(std::ostringstream& o, const Tree& t, int id, const std::stri
     Emitter e{t, o, sh};
     e.words = words;
     std::string m = e.warp(id, 0, "src");
-    if (R >= 64) {
+    if (R >= 64 && comb && words) {
+        o << "        wStoreBetaComb<" << R << ", " << (comb == 2 ? "true" : "false") << ">(bw, beta + " << v.off / 32
+          << ", beta + " << (v.off - R) / 32 << ");\n";
+        if (g_marks) o << "        " << g_marks->mark("StoreBetaComb<" + std::to_string(R) + ">") << "\n";
+    } else if (R >= 64) {
         o << "        wStoreBeta<" << R << ">(bw, beta + " << v.off / 32 << ");\n";
         if (g_marks) o << "        " << g_marks->mark("StoreBeta<" + std::to_string(R) + ">") << "\n";
     } else {
@@ -412,19 +421,23 @@ struct CtaEmitter {
     bool helper = false;                  // HELPER: instruction run-ahead warp (latency variant)
     bool latni = false;                   // latency-copy subtrees non-inlined
     std::vector<std::string> lat_subs;    // latency-copy subtree functions, in call order
+    int comb_req = 0, comb_req_id = -1;   // a Combine the next subtree call (node comb_req_id) performs
+    bool comb_done = false;
     void sub_call(int id, const std::string& src) {
         std::string fname = "sub" + std::to_string(n_subs++);
+        const int comb = (comb_req && comb_req_id == id) ? comb_req : 0;
+        if (comb) comb_done = true;
         if ((sh && !sh->sizes.empty() && sh_lat) || helper || latni) {
             TraceMarks* keep = g_marks;
             g_marks = nullptr;  // trace marks only in the latency copy
-            emit_warp_sub(subs, t, id, fname + "_tp", sh);
+            emit_warp_sub(subs, t, id, fname + "_tp", sh, false, false, comb);
             g_marks = keep;
-            emit_warp_sub(subs, t, id, fname + "_lat", sh_lat ? sh_lat : sh, false, helper || latni);
+            emit_warp_sub(subs, t, id, fname + "_lat", sh_lat ? sh_lat : sh, false, helper || latni, comb);
             lat_subs.push_back(fname + "_lat");
             emit("if constexpr (T == 32) { " + fname + "_tp<P>(" + src + ", beta); } else { if (w0) " +
                  fname + "_lat<P>(" + src + ", beta); }");
         } else {
-            emit_warp_sub(subs, t, id, fname, sh);
+            emit_warp_sub(subs, t, id, fname, sh, false, false, comb);
             emit("if (w0) " + fname + "<P>(" + src + ", beta);");
         }
         emit("sync.sub();");
@@ -454,6 +467,7 @@ struct CtaEmitter {
     // warp-0 region.  Returns the child's first-op kind (OP_F 0, OP_G0R 2) or -1.
     bool fuse = false;
     int fuse_depth = 3;  // FUSE=2: pairs only
+    bool fuse_comb = false;  // FCOMB=1 (spec option): subtree right children perform their parent's Combine
     int fuse_kind(int cid) {
         if (!fuse) return -1;
         const Node& c = t.nodes[cid];
@@ -539,15 +553,30 @@ struct CtaEmitter {
         // done > 0: this node's first op (G_0R or F) ran fused into an ancestor's op, and so did the
         // first ops of done - 1 further nodes down its first-child chain
         // HELPER: one arrive per subtree call, just before the stage op that produces its input
+        // a right child that is a warp subtree performs this node's Combine itself (fuse_comb)
+        auto want_comb = [&](int kind) {
+            comb_req = (fuse_comb && r.kind != Kind::Rate0 && r.n <= W && h >= 64 && h <= 512) ? kind : 0;
+            comb_req_id = v.right;
+            comb_done = false;
+        };
+        auto comb_tail = [&](const std::string& op) {
+            const bool fused = comb_req && comb_done;
+            comb_req = 0;
+            comb_req_id = -1;
+            comb_done = false;
+            if (fused) return;
+            emit(op + "<T, " + N_ + ">(" + B + ");");
+            emit("sync.comb();");
+        };
         if (l.kind == Kind::Rate0) {
+            want_comb(2);
             if (done > 0) {
                 child(v.right, D, done - 1);
             } else {
                 if (helper && h == W && r.kind != Kind::Rate0) emit("if (gtid<T>() < 32) sync.helper_arrive();");
                 xop_child(id, 2, src, D, B, v.right);
             }
-            emit("cComb0R<T, " + N_ + ">(" + B + ");");
-            emit("sync.comb();");
+            comb_tail("cComb0R");
             return;
         }
         if (done > 0) {
@@ -558,9 +587,9 @@ struct CtaEmitter {
         }
         if (r.kind == Kind::Rate0) return;
         if (helper && h == W) emit("if (gtid<T>() < 32) sync.helper_arrive();");
+        want_comb(1);
         xop_child(id, 1, src, D, B, v.right);
-        emit("cComb<T, " + N_ + ">(" + B + ");");
-        emit("sync.comb();");
+        comb_tail("cComb");
     }
 };
 
@@ -790,6 +819,7 @@ void emit_code(const Spec& sp, const std::string& outdir, std::ostringstream& re
         ce.latni = sp.latni;
         ce.fuse = sp.fuse >= 2 && !ce.helper;
         ce.fuse_depth = sp.fuse;
+        ce.fuse_comb = sp.fcomb && !ce.helper;
         int acc = 0, sacc = 0, gacc = 0, hs = 0, hg = 0;
         const int gs = sp.gs > 0 ? sp.gs : (sp.N >= 16384 ? sp.N / 4 : sp.N + 1);
         ce.h16 = sp.h16;
@@ -1124,6 +1154,7 @@ void parse_options(Spec& sp, std::istream& ls) {
             else if (opt.rfind("XWPC=", 0) == 0) sp.xwpc = std::atoi(opt.c_str() + 5);
             else if (opt.rfind("GBETA=", 0) == 0) sp.gbeta = std::atoi(opt.c_str() + 6) != 0;
             else if (opt.rfind("FUSE=", 0) == 0) sp.fuse = std::atoi(opt.c_str() + 5);
+            else if (opt.rfind("FCOMB=", 0) == 0) sp.fcomb = std::atoi(opt.c_str() + 6) != 0;
             else if (opt.rfind("DEDUP=", 0) == 0) {  // comma-separated sizes, or "none"
                 sp.dedup.clear();
                 std::stringstream ds(opt.substr(6));

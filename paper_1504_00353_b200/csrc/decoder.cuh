@@ -828,6 +828,35 @@ PD_INLINE void wStoreBeta(const BW<NW>& bw, uint32_t* words) {
         }
     }
 }
+// A subtree that is the right child of a CTA-level node also performs that node's Combine
+// (eq:combine P:318-325) while its words are still in registers: left words ^= right words, or
+// left = right for Combine_0R (ZL, the left child was Rate-0 and left its words zero).  Replaces
+// the CTA-level combine op and its barrier.
+template <int R, bool ZL, int NW>
+PD_INLINE void wStoreBetaComb(const BW<NW>& bw, uint32_t* words, uint32_t* left) {
+    static_assert(R / 32 == NW, "");
+    if (lane_id() == 0) {
+        if constexpr (NW >= 4) {
+#pragma unroll
+            for (int g = 0; g < NW / 4; ++g) {
+                const uint4 r = make_uint4(bw.w[4 * g], bw.w[4 * g + 1], bw.w[4 * g + 2], bw.w[4 * g + 3]);
+                *reinterpret_cast<uint4*>(words + 4 * g) = r;
+                if constexpr (ZL) {
+                    *reinterpret_cast<uint4*>(left + 4 * g) = r;
+                } else {
+                    const uint4 l = *reinterpret_cast<const uint4*>(left + 4 * g);
+                    *reinterpret_cast<uint4*>(left + 4 * g) = make_uint4(l.x ^ r.x, l.y ^ r.y, l.z ^ r.z, l.w ^ r.w);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < NW; ++k) {
+                words[k] = bw.w[k];
+                left[k] = ZL ? bw.w[k] : (left[k] ^ bw.w[k]);
+            }
+        }
+    }
+}
 // shared subtree functions of 64 values return their two words packed in 64 bits
 template <int s0, int NW>
 PD_INLINE void wSetWords64(BW<NW>& bw, uint64_t m) {
