@@ -1181,7 +1181,7 @@ bool codegen_jit(int N, int K, const uint8_t* frozen, JitCode* out, std::string*
     std::istringstream opts(N >= 16384 ? "W=512 FPC=6 CPS=3 DEDUP=32"
                             : N == 8192 ? "W=512 T=512 GS=2048 DEDUP=16,32,64"
                             : N == 4096 ? "W=1024 T=256"
-                            : N == 2048 ? "W=2048 WLAT=1024 FPC=8 CPS=2"
+                            : N == 2048 ? "W=256 WF=2048 WLAT=1024 FPC=8 CPS=2"
                                         : "");
     parse_options(sp, opts);
     std::ostringstream decl, entries;
