@@ -248,8 +248,11 @@ struct Emitter {
         std::string ml = warp(v.left, off, csrc, child);
         if (h == 32 && ml != "0u") o << ind << "wDeposit<" << s0 << ">(bw, " << ml << ");\n";
         if (r.kind == Kind::Rate0) return n <= 32 ? ml : "";
-        o << ind << "wG<P, " << N_ << ", " << S0 << ">(" << src << ", " << child << ", bw, "
-          << (n <= 32 ? ml : std::string("0u")) << ");\n";
+        if (n <= 32 && l.kind == Kind::Rep)  // the left mask is all ones or zero: uniform sign
+            o << ind << "wGu<P, " << N_ << ">(" << src << ", " << child << ", " << ml << ");\n";
+        else
+            o << ind << "wG<P, " << N_ << ", " << S0 << ">(" << src << ", " << child << ", bw, "
+              << (n <= 32 ? ml : std::string("0u")) << ");\n";
         mk("G<" + N_ + ">");
         std::string mr = warp(v.right, off + h, csrc, child);
         if (n <= 32) {

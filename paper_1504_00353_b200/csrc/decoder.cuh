@@ -562,6 +562,22 @@ PD_INLINE void wG(const Src& s, typename P::v_t* c, uint64_t bw, uint32_t ml) {
     PD_DUMPR(n, c);
 }
 
+// G<n> (n <= 32) after a repetition left child: its mask ml is all ones or zero, so the sign
+// is bit 0 of ml moved to bit 31 -- no per-lane bit extraction on the critical path.
+template <class P, int n, class Src>
+PD_INLINE void wGu(const Src& s, typename P::v_t* c, uint32_t ml) {
+    static_assert(n <= 32, "");
+    constexpr int LH = n == 2 ? 0 : n == 4 ? 1 : n == 8 ? 2 : n == 16 ? 3 : 4;
+    const uint32_t sgn = ml << 31;
+    const uint32_t sec = lane_id() << (31 - LH);
+    typename P::v_t x, y;
+    s.pair(n / 2, x, y);
+    const float xa = __uint_as_float(__float_as_uint(x) ^ (sgn & ~sec));
+    const float ya = __uint_as_float(__float_as_uint(y) ^ (sgn & sec));
+    c[0] = P::g0(xa, ya);
+    PD_DUMPR(n, c);
+}
+
 // G_0R<n>: G with beta_l = 0 (left child Rate-0); b + a is symmetric.
 template <class P, int n, class Src>
 PD_INLINE void wG0R(const Src& s, typename P::v_t* c) {
