@@ -631,8 +631,10 @@ PD_INLINE bool wRepDecide(const Src& s) {
         // (1.5 * 2^23 magic) and one redux.sync.add sums the warp: the node's sum (N_v >= 64) or
         // 32 / N_v copies of it (replicated N_v <= 32) -- the same sign, hence the same decision
         // (C9, C12) -- one 23-cycle collective instead of log2(N_v) dependent shuffle-adds
-        const int iv = __float_as_int(t0 + 12582912.0f) - 0x4B400000;
-        return __reduce_add_sync(FULL, iv) < 0;
+        // (the 32 magic offsets are left in: the sum is 0x68000000 + sum mod 2^32, and for
+        // |sum| < 2^26 the sum is negative exactly when that is below 0x68000000, unsigned)
+        const uint32_t tot = __reduce_add_sync(FULL, (uint32_t)__float_as_int(t0 + 12582912.0f));
+        return tot < 0x68000000u;
     } else {
 #pragma unroll
         for (int o = start; o >= 1; o /= 2) t0 = P::add(t0, __shfl_xor_sync(FULL, t0, o));
